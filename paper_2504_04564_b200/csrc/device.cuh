@@ -1,0 +1,407 @@
+// device.cuh — sm_100a device layout of the frozen {5,4,3} tree and the per-thread hot path:
+// cached accessor, N-bit leaf decode, trilinear reconstruction, transfer function, splitmix64
+// streams and the macrocell DDA. Semantics follow the reference exactly (file:line per function,
+// paths under /root/reference/proj/include/svdb/). Translation units including this header are
+// compiled with -fmad=false so every FP64 expression rounds like the reference's x86-64 build;
+// the only fused op is the explicit fmaf() of the affine leaf decode (bit-identical to C99 fmaf).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "layout.hpp"
+
+namespace svdbgpu {
+
+// ---- TreeConfig slot math (tree.hpp:43-71) ----
+__device__ __forceinline__ int upper_slot(int x, int y, int z)
+{
+    return ((x >> 7) & 31) + 32 * (((y >> 7) & 31) + 32 * ((z >> 7) & 31));
+}
+__device__ __forceinline__ int lower_slot(int x, int y, int z)
+{
+    return ((x >> 3) & 15) + 16 * (((y >> 3) & 15) + 16 * ((z >> 3) & 15));
+}
+__device__ __forceinline__ int leaf_voxel(int x, int y, int z)
+{
+    return (x & 7) + 8 * ((y & 7) + 8 * (z & 7));
+}
+
+// ---- leaf decode ----
+template <int CODEC>
+__device__ __forceinline__ float decode(const DevGrid& g, uint32_t leaf, int vi, float lo, float sc)
+{
+    const uint8_t* base = g.codes + size_t(leaf) * g.leaf_stride;
+    if constexpr (CODEC == kCodecF32) {
+        return __ldg(reinterpret_cast<const float*>(base) + vi);
+    } else if constexpr (CODEC == kCodecUnorm8) {
+        // == (float)code / 255.0f for every code (exhaustively checked, tests/test_codec.py)
+        return __double2float_rn(double(__ldg(base + vi)) * (1.0 / 255.0));
+    } else if constexpr (CODEC == kCodecAffine8) {
+        return fmaf(float(__ldg(base + vi)), sc, lo);
+    } else {
+        uint32_t b = __ldg(base + (vi >> 1));
+        return fmaf(float((b >> ((vi & 1) * 4)) & 15u), sc, lo);
+    }
+}
+
+// std::lower_bound over the zyx-sorted root (frozen.hpp:101-110), libstdc++ probe order.
+__device__ __forceinline__ int find_upper(const DevGrid& g, int ox, int oy, int oz)
+{
+    int lo = 0, len = g.n_root;
+    while (len > 0) {
+        int half = len >> 1;
+        int4 e = __ldg(g.root + lo + half);
+        bool less = e.z != oz ? e.z < oz : (e.y != oy ? e.y < oy : e.x < ox);
+        if (less) {
+            lo = lo + half + 1;
+            len = len - half - 1;
+        } else {
+            len = half;
+        }
+    }
+    if (lo == g.n_root)
+        return -1;
+    int4 e = __ldg(g.root + lo);
+    return (e.x == ox && e.y == oy && e.z == oz) ? e.w : -1;
+}
+
+// Per-thread read-through cache (Accessor, frozen.hpp:228-277). Keys are the coordinate-derived
+// node origins; values never depend on the cache state (test_tree.cpp:247-271).
+template <int CODEC>
+struct Accessor {
+    const DevGrid* g;
+    int lx, ly, lz; // cached leaf origin
+    uint32_t leaf;
+    float lo, sc;
+    int wx, wy, wz; // cached lower origin
+    uint32_t lower;
+    int ux, uy, uz; // cached upper origin
+    int upper;      // -1: no upper node there
+
+    __device__ __forceinline__ explicit Accessor(const DevGrid& grid) : g(&grid)
+    {
+        // odd origins never equal an aligned node origin: all three caches start cold
+        lx = ly = lz = 1;
+        wx = wy = wz = 1;
+        ux = uy = uz = 1;
+        leaf = lower = 0;
+        lo = sc = 0.0f;
+        upper = -1;
+    }
+
+    __device__ __forceinline__ float read_lower(int x, int y, int z)
+    {
+        uint4 e = __ldg(g->lower + size_t(lower) * 4096 + lower_slot(x, y, z));
+        if (e.x == kSlotTile)
+            return __uint_as_float(e.y);
+        if (e.x != kSlotChild)
+            return g->background;
+        lx = x & ~7;
+        ly = y & ~7;
+        lz = z & ~7;
+        leaf = e.y;
+        lo = __uint_as_float(e.z);
+        sc = __uint_as_float(e.w);
+        return decode<CODEC>(*g, leaf, leaf_voxel(x, y, z), lo, sc);
+    }
+
+    __device__ __forceinline__ float read_upper(int x, int y, int z)
+    {
+        uint2 e = __ldg(g->upper + size_t(upper) * 32768 + upper_slot(x, y, z));
+        if (e.x == kSlotTile)
+            return __uint_as_float(e.y);
+        if (e.x != kSlotChild)
+            return g->background;
+        wx = x & ~127;
+        wy = y & ~127;
+        wz = z & ~127;
+        lower = e.y;
+        return read_lower(x, y, z);
+    }
+
+    __device__ __forceinline__ bool in_leaf(int x, int y, int z) const
+    {
+        return (x & ~7) == lx && (y & ~7) == ly && (z & ~7) == lz;
+    }
+
+    __device__ __forceinline__ float read(int x, int y, int z)
+    {
+        if (in_leaf(x, y, z))
+            return decode<CODEC>(*g, leaf, leaf_voxel(x, y, z), lo, sc);
+        if ((x & ~127) == wx && (y & ~127) == wy && (z & ~127) == wz)
+            return read_lower(x, y, z);
+        int ox = x & ~4095, oy = y & ~4095, oz = z & ~4095;
+        if (!(ox == ux && oy == uy && oz == uz)) {
+            ux = ox;
+            uy = oy;
+            uz = oz;
+            upper = find_upper(*g, ox, oy, oz);
+            wx = 1; // invalidate the lower cache
+        }
+        if (upper < 0)
+            return g->background;
+        return read_upper(x, y, z);
+    }
+};
+
+// Uncached root-to-leaf walk (FrozenGrid::read_voxel, frozen.hpp:82-99).
+template <int CODEC>
+__device__ float read_voxel(const DevGrid& g, int x, int y, int z)
+{
+    int u = find_upper(g, x & ~4095, y & ~4095, z & ~4095);
+    if (u < 0)
+        return g.background;
+    uint2 ue = __ldg(g.upper + size_t(u) * 32768 + upper_slot(x, y, z));
+    if (ue.x == kSlotTile)
+        return __uint_as_float(ue.y);
+    if (ue.x != kSlotChild)
+        return g.background;
+    uint4 le = __ldg(g.lower + size_t(ue.y) * 4096 + lower_slot(x, y, z));
+    if (le.x == kSlotTile)
+        return __uint_as_float(le.y);
+    if (le.x != kSlotChild)
+        return g.background;
+    return decode<CODEC>(g, le.y, leaf_voxel(x, y, z), __uint_as_float(le.z), __uint_as_float(le.w));
+}
+
+// ---- sampler (sample.hpp:24-72) ----
+__device__ __forceinline__ int lattice_coord(double v)
+{
+    double f = floor(v);
+    if (f < -1.0e9)
+        return -1000000000;
+    if (f > 1.0e9)
+        return 1000000000;
+    return int(f);
+}
+
+template <int CODEC>
+__device__ __forceinline__ float sample_trilinear(Accessor<CODEC>& a, double px, double py, double pz)
+{
+    int x0 = lattice_coord(px), y0 = lattice_coord(py), z0 = lattice_coord(pz);
+    double wx = px - floor(px), wy = py - floor(py), wz = pz - floor(pz);
+    double v000, v100, v010, v110, v001, v101, v011, v111;
+    v000 = a.read(x0, y0, z0);
+    if (((x0 & 7) != 7) & ((y0 & 7) != 7) & ((z0 & 7) != 7) & a.in_leaf(x0, y0, z0)) {
+        // all eight taps inside the cached leaf: decode directly, no node walk
+        int vi = leaf_voxel(x0, y0, z0);
+        v100 = decode<CODEC>(*a.g, a.leaf, vi + 1, a.lo, a.sc);
+        v010 = decode<CODEC>(*a.g, a.leaf, vi + 8, a.lo, a.sc);
+        v110 = decode<CODEC>(*a.g, a.leaf, vi + 9, a.lo, a.sc);
+        v001 = decode<CODEC>(*a.g, a.leaf, vi + 64, a.lo, a.sc);
+        v101 = decode<CODEC>(*a.g, a.leaf, vi + 65, a.lo, a.sc);
+        v011 = decode<CODEC>(*a.g, a.leaf, vi + 72, a.lo, a.sc);
+        v111 = decode<CODEC>(*a.g, a.leaf, vi + 73, a.lo, a.sc);
+    } else {
+        v100 = a.read(x0 + 1, y0, z0);
+        v010 = a.read(x0, y0 + 1, z0);
+        v110 = a.read(x0 + 1, y0 + 1, z0);
+        v001 = a.read(x0, y0, z0 + 1);
+        v101 = a.read(x0 + 1, y0, z0 + 1);
+        v011 = a.read(x0, y0 + 1, z0 + 1);
+        v111 = a.read(x0 + 1, y0 + 1, z0 + 1);
+    }
+    double v00 = v000 * (1.0 - wx) + v100 * wx;
+    double v10 = v010 * (1.0 - wx) + v110 * wx;
+    double v01 = v001 * (1.0 - wx) + v101 * wx;
+    double v11 = v011 * (1.0 - wx) + v111 * wx;
+    double v0 = v00 * (1.0 - wy) + v10 * wy;
+    double v1 = v01 * (1.0 - wy) + v11 * wy;
+    return float(v0 * (1.0 - wz) + v1 * wz);
+}
+
+template <int CODEC>
+__device__ __forceinline__ float sample_nearest(Accessor<CODEC>& a, double px, double py, double pz)
+{
+    return a.read(lattice_coord(px + 0.5), lattice_coord(py + 0.5), lattice_coord(pz + 0.5));
+}
+
+// ---- transfer function (transfer.hpp:47-91); entries in shared memory ----
+__device__ __forceinline__ double dclamp(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
+
+__device__ __forceinline__ double tf_normalized(const DevTF& tf, double v)
+{
+    return dclamp((v - tf.lo) / (tf.hi - tf.lo), 0.0, 1.0);
+}
+
+__device__ __forceinline__ void tf_lookup(const DevTF& tf, const float4* ent, double v, double out[4])
+{
+    double u = tf_normalized(tf, v) * double(tf.n - 1);
+    unsigned long long i0 = (unsigned long long)u;
+    if ((unsigned long long)(tf.n - 2) < i0)
+        i0 = (unsigned long long)(tf.n - 2);
+    double t = u - double(i0);
+    float4 a = ent[i0], b = ent[i0 + 1];
+    out[0] = (1.0 - t) * double(a.x) + t * double(b.x);
+    out[1] = (1.0 - t) * double(a.y) + t * double(b.y);
+    out[2] = (1.0 - t) * double(a.z) + t * double(b.z);
+    out[3] = (1.0 - t) * double(a.w) + t * double(b.w);
+}
+
+__device__ __forceinline__ double tf_alpha(const DevTF& tf, const float4* ent, double v)
+{
+    double u = tf_normalized(tf, v) * double(tf.n - 1);
+    unsigned long long i0 = (unsigned long long)u;
+    if ((unsigned long long)(tf.n - 2) < i0)
+        i0 = (unsigned long long)(tf.n - 2);
+    double t = u - double(i0);
+    return (1.0 - t) * double(ent[i0].w) + t * double(ent[i0 + 1].w);
+}
+
+__device__ __forceinline__ double tf_extinction(const DevTF& tf, const float4* ent, double v)
+{
+    return tf.scale * tf_alpha(tf, ent, v);
+}
+
+__device__ __forceinline__ double tf_max_alpha_in_range(const DevTF& tf, const float4* ent, double vlo, double vhi)
+{
+    if (vhi < vlo) {
+        double t = vlo;
+        vlo = vhi;
+        vhi = t;
+    }
+    double m = dmax(tf_alpha(tf, ent, vlo), tf_alpha(tf, ent, vhi));
+    double ulo = tf_normalized(tf, vlo), uhi = tf_normalized(tf, vhi);
+    for (int i = 0; i < tf.n; ++i) {
+        double u = double(i) / double(tf.n - 1);
+        if (u > ulo && u < uhi)
+            m = dmax(m, double(ent[i].w));
+    }
+    return m;
+}
+
+// ---- splitmix64 streams (rng.hpp:12-67) ----
+__device__ __forceinline__ uint64_t mix64(uint64_t x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+struct Rng {
+    uint64_t state;
+    __device__ __forceinline__ static Rng for_pixel_sample(uint64_t seed_mixed, int px, int py, int s)
+    {
+        // seed_mixed = mix64(seed), hoisted to the host
+        uint64_t h = mix64(seed_mixed ^ ((uint64_t(uint32_t(px)) << 32) | uint32_t(py)));
+        h = mix64(h ^ uint64_t(uint32_t(s)));
+        return Rng{mix64(h)};
+    }
+    __device__ __forceinline__ double uniform()
+    {
+        state += 0x9E3779B97F4A7C15ull;
+        uint64_t x = state;
+        x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+        x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+        x ^= x >> 31;
+        return double(x >> 11) * 0x1.0p-53;
+    }
+};
+
+// ---- macrocell DDA (dda.hpp:25-109) ----
+struct Ray {
+    double o[3], d[3];
+};
+
+__device__ __forceinline__ bool clip_ray_box(const Ray& r, const double hi[3], double& t0, double& t1)
+{
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double o = r.o[a], d = r.d[a];
+        if (d == 0.0) {
+            if (o < 0.0 || o > hi[a])
+                return false;
+            continue;
+        }
+        double inv = 1.0 / d;
+        double ta = (0.0 - o) * inv, tb = (hi[a] - o) * inv;
+        if (ta > tb) {
+            double t = ta;
+            ta = tb;
+            tb = t;
+        }
+        t0 = dmax(t0, ta);
+        t1 = dmin(t1, tb);
+        if (t0 > t1)
+            return false;
+    }
+    return true;
+}
+
+struct Dda {
+    int c[3], step[3];
+    double t_next[3], t_delta[3], t_cur, t1;
+    bool done;
+
+    __device__ __forceinline__ bool init(const int cells[3], const double hi[3], const Ray& r, double t0_, double t1_)
+    {
+        double t0 = t0_;
+        t1 = t1_;
+        if (!clip_ray_box(r, hi, t0, t1))
+            return false;
+        if (!(t0 <= t1))
+            return false;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            double e = r.o[a] + r.d[a] * t0;
+            c[a] = int(dclamp(floor(e / 32.0), 0.0, double(cells[a] - 1)));
+            double d = r.d[a];
+            step[a] = 0;
+            t_next[a] = __longlong_as_double(0x7ff0000000000000ll);
+            t_delta[a] = t_next[a];
+            if (d > 0.0) {
+                step[a] = 1;
+                t_next[a] = (double(c[a] + 1) * 32.0 - r.o[a]) / d;
+                t_delta[a] = 32.0 / d;
+            } else if (d < 0.0) {
+                step[a] = -1;
+                t_next[a] = (double(c[a]) * 32.0 - r.o[a]) / d;
+                t_delta[a] = -32.0 / d;
+            }
+        }
+        t_cur = t0;
+        done = false;
+        return true;
+    }
+
+    // Next visit (cell, ta, tb); false when traversal has ended.
+    __device__ __forceinline__ bool next(const int cells[3], int cell[3], double& ta, double& tb)
+    {
+        if (done)
+            return false;
+        int axis = 0;
+        if (t_next[1] < t_next[axis])
+            axis = 1;
+        if (t_next[2] < t_next[axis])
+            axis = 2;
+        double tn = axis == 0 ? t_next[0] : (axis == 1 ? t_next[1] : t_next[2]);
+        double t_exit = dmin(tn, t1);
+        t_exit = dmax(t_exit, t_cur);
+        cell[0] = c[0];
+        cell[1] = c[1];
+        cell[2] = c[2];
+        ta = t_cur;
+        tb = t_exit;
+        if (t_exit >= t1) {
+            done = true;
+            return true;
+        }
+        t_cur = t_exit;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            if (a == axis) {
+                c[a] += step[a];
+                if (c[a] < 0 || c[a] >= cells[a])
+                    done = true;
+                else
+                    t_next[a] += t_delta[a];
+            }
+        return true;
+    }
+};
+
+} // namespace svdbgpu

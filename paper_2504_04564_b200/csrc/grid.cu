@@ -1,0 +1,575 @@
+// grid.cu — device layout build (K0), lattice lookups (K1/K2) and macrocell ranges/majorants (K3).
+//
+//   K0 grid_create      <- parse_frozen (io.hpp:183-256) + device relayout / leaf codec
+//   K1 k_read_voxels    <- FrozenGrid::read_voxel (frozen.hpp:82-99)
+//   K2 k_sample         <- sample(Accessor, p, mode) (sample.hpp:97-100), gradient (sample.hpp:81-95)
+//   K3 k_cell_ranges    <- build_macrocells (macrocell.hpp:74-103)
+//      k_majorants      <- update_majorants (macrocell.hpp:108-116)
+#include "device.cuh"
+#include "grid_impl.hpp"
+
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+namespace svdbgpu {
+
+namespace {
+
+constexpr uint64_t kHdr = 72, kRootRec = 16;
+constexpr uint64_t kUpperRec = 16 + 4ull * 32768 + 2ull * 4096;
+constexpr uint64_t kLowerRec = 16 + 4ull * 4096 + 2ull * 512;
+constexpr uint64_t kLeafRec = 16 + 64 + 4ull * 512;
+
+inline uint32_t rd_u32(const uint8_t* p) { uint32_t v; std::memcpy(&v, p, 4); return v; }
+inline int32_t rd_i32(const uint8_t* p) { int32_t v; std::memcpy(&v, p, 4); return v; }
+inline uint64_t rd_u64(const uint8_t* p) { uint64_t v; std::memcpy(&v, p, 8); return v; }
+inline float rd_f32(const uint8_t* p) { float v; std::memcpy(&v, p, 4); return v; }
+inline bool bit(const uint8_t* words, int i) { return (rd_u64(words + 8 * (i >> 6)) >> (i & 63)) & 1u; }
+
+// ---- K0: leaf codec, one warp per leaf, 128-bit coalesced loads of the staged records ----
+template <int CODEC>
+__global__ void __launch_bounds__(256) k_leaf_encode(const uint8_t* __restrict__ staging, uint64_t n_leaf,
+                                                     uint8_t* __restrict__ codes, float2* __restrict__ params,
+                                                     int* __restrict__ bad)
+{
+    const int lane = threadIdx.x & 31;
+    const uint64_t leaf = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (leaf >= n_leaf)
+        return;
+    const float4* vals = reinterpret_cast<const float4*>(staging + leaf * kLeafRec + 80);
+    float4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        v[j] = __ldg(vals + j * 32 + lane); // floats [4(32j+lane), +4): 512 B per warp step
+    if constexpr (CODEC == kCodecF32) {
+        float4* dst = reinterpret_cast<float4*>(codes + leaf * 2048);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            dst[j * 32 + lane] = v[j];
+        if (lane == 0)
+            params[leaf] = make_float2(0.0f, 0.0f);
+        return;
+    } else if constexpr (CODEC == kCodecUnorm8) {
+        uint32_t* dst = reinterpret_cast<uint32_t*>(codes + leaf * 512);
+        bool ok = true;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float f[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+            uint32_t w = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                int c = __float2int_rn(__fmul_rn(f[k], 255.0f));
+                ok &= f[k] >= 0.0f && f[k] <= 1.0f && c >= 0 && c <= 255 &&
+                      __double2float_rn(double(c) * (1.0 / 255.0)) == f[k];
+                w |= uint32_t(c & 255) << (8 * k);
+            }
+            dst[j * 32 + lane] = w;
+        }
+        if (!ok)
+            atomicExch(bad, 1);
+        if (lane == 0)
+            params[leaf] = make_float2(0.0f, 0.0f);
+        return;
+    } else {
+        constexpr int levels = CODEC == kCodecAffine8 ? 255 : 15;
+        float lo = v[0].x, hi = v[0].x;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            lo = fminf(lo, fminf(fminf(v[j].x, v[j].y), fminf(v[j].z, v[j].w)));
+            hi = fmaxf(hi, fmaxf(fmaxf(v[j].x, v[j].y), fmaxf(v[j].z, v[j].w)));
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+        }
+        if (lo == 0.0f)
+            lo = 0.0f; // canonical +0 (the oracle does the same)
+        if (hi == 0.0f)
+            hi = 0.0f;
+        const float scale = hi > lo ? __fdiv_rn(__fsub_rn(hi, lo), float(levels)) : 0.0f;
+        auto q = [&](float x) -> uint32_t {
+            if (!(scale > 0.0f))
+                return 0u;
+            float r = floorf(__fadd_rn(__fdiv_rn(__fsub_rn(x, lo), scale), 0.5f));
+            return r < 0.0f ? 0u : (r > float(levels) ? uint32_t(levels) : uint32_t(r));
+        };
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t c0 = q(v[j].x), c1 = q(v[j].y), c2 = q(v[j].z), c3 = q(v[j].w);
+            if constexpr (CODEC == kCodecAffine8) {
+                reinterpret_cast<uint32_t*>(codes + leaf * 512)[j * 32 + lane] =
+                    c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+            } else {
+                reinterpret_cast<uint16_t*>(codes + leaf * 256)[j * 32 + lane] =
+                    uint16_t(c0 | (c1 << 4) | (c2 << 8) | (c3 << 12));
+            }
+        }
+        if (lane == 0)
+            params[leaf] = make_float2(lo, scale);
+    }
+}
+
+// Lower slot table with the child leaf's decode parameters folded in (one 16-B load per miss).
+__global__ void k_expand_lower(const uint2* __restrict__ staged, uint64_t n_slots,
+                               const float2* __restrict__ params, uint4* __restrict__ lower)
+{
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_slots;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        uint2 e = staged[i];
+        uint4 o = make_uint4(e.x, e.y, 0u, 0u);
+        if (e.x == kSlotChild) {
+            float2 p = params[e.y];
+            o.z = __float_as_uint(p.x);
+            o.w = __float_as_uint(p.y);
+        }
+        lower[i] = o;
+    }
+}
+
+// ---- K1 ----
+template <int CODEC>
+__global__ void k_read_voxels(DevGrid g, const int32_t* __restrict__ ijk, size_t n, float* __restrict__ out)
+{
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        out[i] = read_voxel<CODEC>(g, ijk[3 * i], ijk[3 * i + 1], ijk[3 * i + 2]);
+}
+
+// ---- K2 ----
+template <int CODEC>
+__global__ void k_sample(DevGrid g, const double* __restrict__ xyz, size_t n, int mode, float* __restrict__ out)
+{
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        Accessor<CODEC> a(g);
+        double x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+        out[i] = mode == 0 ? sample_nearest<CODEC>(a, x, y, z) : sample_trilinear<CODEC>(a, x, y, z);
+    }
+}
+
+template <int CODEC>
+__global__ void k_gradient(DevGrid g, const double* __restrict__ xyz, size_t n, double* __restrict__ out)
+{
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        Accessor<CODEC> a(g);
+        double x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+        const double h = 0.5;
+        out[3 * i] = (double(sample_trilinear<CODEC>(a, x + h, y, z)) - double(sample_trilinear<CODEC>(a, x - h, y, z))) / (2.0 * h);
+        out[3 * i + 1] = (double(sample_trilinear<CODEC>(a, x, y + h, z)) - double(sample_trilinear<CODEC>(a, x, y - h, z))) / (2.0 * h);
+        out[3 * i + 2] = (double(sample_trilinear<CODEC>(a, x, y, z + h)) - double(sample_trilinear<CODEC>(a, x, y, z - h))) / (2.0 * h);
+    }
+}
+
+// ---- K3: exact closed-box ranges, one CTA per 32^3 cell (33^3 voxels incl. shared layer) ----
+template <int CODEC>
+__global__ void __launch_bounds__(256) k_cell_ranges(DevGrid g, int cx_n, int cy_n, float* __restrict__ cmin,
+                                                     float* __restrict__ cmax)
+{
+    const int cell = blockIdx.x;
+    const int cx = cell % cx_n, cy = (cell / cx_n) % cy_n, cz = cell / (cx_n * cy_n);
+    const int x0 = cx * 32, y0 = cy * 32, z0 = cz * 32;
+    const int ex = min(x0 + 32, g.dims[0] - 1) - x0 + 1;
+    const int ey = min(y0 + 32, g.dims[1] - 1) - y0 + 1;
+    const int ez = min(z0 + 32, g.dims[2] - 1) - z0 + 1;
+    Accessor<CODEC> a(g);
+    float mn = __int_as_float(0x7f800000), mx = -mn;
+    const int total = ex * ey * ez;
+    // thread t walks x-rows so consecutive reads stay in the cached leaf
+    for (int r = threadIdx.x; r < ey * ez; r += blockDim.x) {
+        int y = y0 + r % ey, z = z0 + r / ey;
+        for (int x = x0; x < x0 + ex; ++x) {
+            float v = a.read(x, y, z);
+            mn = v < mn ? v : mn;
+            mx = mx < v ? v : mx;
+        }
+    }
+    (void)total;
+    __shared__ float smn[8], smx[8];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        float o = __shfl_xor_sync(0xffffffffu, mn, off);
+        mn = o < mn ? o : mn;
+        o = __shfl_xor_sync(0xffffffffu, mx, off);
+        mx = mx < o ? o : mx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        smn[threadIdx.x >> 5] = mn;
+        smx[threadIdx.x >> 5] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+            mn = smn[w] < mn ? smn[w] : mn;
+            mx = mx < smx[w] ? smx[w] : mx;
+        }
+        cmin[cell] = mn;
+        cmax[cell] = mx;
+    }
+}
+
+__global__ void k_majorants(DevTF tf, const float4* __restrict__ ent_g, const float* __restrict__ cmin,
+                            const float* __restrict__ cmax, int n, float* __restrict__ maj,
+                            uint8_t* __restrict__ empty)
+{
+    extern __shared__ float4 ent[];
+    for (int i = threadIdx.x; i < tf.n; i += blockDim.x)
+        ent[i] = ent_g[i];
+    __syncthreads();
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    double m = tf.scale * tf_max_alpha_in_range(tf, ent, double(cmin[i]), double(cmax[i]));
+    maj[i] = float(m);
+    if (empty)
+        empty[i] = m == 0.0 ? 1 : 0;
+}
+
+int grid_blocks(size_t n, int threads = 256)
+{
+    size_t b = (n + threads - 1) / threads;
+    return int(b < 148 * 64 ? (b ? b : 1) : 148 * 64);
+}
+
+} // namespace
+
+int cuda_fail(cudaError_t e, const char* what)
+{
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+        return fail_code(SVDBGPU_E_NO_DEVICE, std::string("no CUDA device (no CPU fallback): ") + cudaGetErrorString(e));
+    if (e == cudaErrorMemoryAllocation)
+        return fail_code(SVDBGPU_E_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+    return fail_code(SVDBGPU_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+GridImpl::~GridImpl()
+{
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaFree(d_root);
+    cudaFree(d_upper);
+    cudaFree(d_lower);
+    cudaFree(d_codes);
+    cudaFree(d_cmin);
+    cudaFree(d_cmax);
+    cudaFree(d_maj);
+    cudaFree(d_tf);
+    cudaFree(d_img);
+    cudaFree(d_counters);
+    cudaFree(d_scratch);
+    if (ev0)
+        cudaEventDestroy(ev0);
+    if (ev1)
+        cudaEventDestroy(ev1);
+    if (stream)
+        cudaStreamDestroy(stream);
+    cudaSetDevice(prev);
+}
+
+int validate_tf(const svdbgpu_tf* tf)
+{
+    // TransferFunction ctor (transfer.hpp:23-35)
+    if (!tf || !tf->rgba)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "transfer function is null");
+    if (!(tf->domain_hi > tf->domain_lo))
+        return fail(Errc::size_mismatch, "transfer function domain must have hi > lo");
+    if (tf->n_entries < 2)
+        return fail(Errc::size_mismatch, "transfer function needs at least 2 entries");
+    if (!(tf->density_scale > 0.0) || !std::isfinite(tf->density_scale))
+        return fail(Errc::size_mismatch, "density_scale must be positive");
+    for (int i = 0; i < tf->n_entries; ++i) {
+        float a = tf->rgba[4 * i + 3];
+        if (!(a >= 0.0f && a <= 1.0f))
+            return fail(Errc::size_mismatch, "transfer function alpha must be in [0,1]");
+    }
+    return 0;
+}
+
+int GridImpl::upload_tf(const svdbgpu_tf* tf, cudaStream_t s, DevTF* out)
+{
+    if (int rc = validate_tf(tf))
+        return rc;
+    if (tf->n_entries > tf_cap) {
+        cudaFree(d_tf);
+        d_tf = nullptr;
+        SVDB_CUDA(cudaMalloc(&d_tf, sizeof(float4) * size_t(tf->n_entries)));
+        tf_cap = tf->n_entries;
+    }
+    SVDB_CUDA(cudaMemcpyAsync(d_tf, tf->rgba, sizeof(float4) * size_t(tf->n_entries), cudaMemcpyHostToDevice, s));
+    *out = DevTF{tf->domain_lo, tf->domain_hi, tf->density_scale, tf->n_entries};
+    return 0;
+}
+
+#define SVDB_CODEC_DISPATCH(codec, F)                                                         \
+    switch (codec) {                                                                           \
+    case kCodecF32: F(kCodecF32); break;                                                       \
+    case kCodecUnorm8: F(kCodecUnorm8); break;                                                 \
+    case kCodecAffine8: F(kCodecAffine8); break;                                               \
+    default: F(kCodecAffine4); break;                                                          \
+    }
+
+int GridImpl::ensure_ranges(cudaStream_t s, float* ms)
+{
+    if (ranges_valid) {
+        if (ms)
+            *ms = 0.0f;
+        return 0;
+    }
+    for (int a = 0; a < 3; ++a)
+        cells[a] = std::max(1, (dg.dims[a] - 1 + 31) / 32); // cell_counts_for (macrocell.hpp:66-70)
+    size_t nc = size_t(cells[0]) * cells[1] * cells[2];
+    SVDB_CUDA(cudaMalloc(&d_cmin, nc * 4));
+    SVDB_CUDA(cudaMalloc(&d_cmax, nc * 4));
+    SVDB_CUDA(cudaMalloc(&d_maj, nc * 4));
+    SVDB_CUDA(cudaEventRecord(ev0, s));
+#define LAUNCH_RANGES(C) k_cell_ranges<C><<<unsigned(nc), 256, 0, s>>>(dg, cells[0], cells[1], d_cmin, d_cmax)
+    SVDB_CODEC_DISPATCH(codec, LAUNCH_RANGES)
+#undef LAUNCH_RANGES
+    SVDB_CUDA(cudaGetLastError());
+    SVDB_CUDA(cudaEventRecord(ev1, s));
+    SVDB_CUDA(cudaEventSynchronize(ev1));
+    float t = 0.0f;
+    cudaEventElapsedTime(&t, ev0, ev1);
+    if (ms)
+        *ms = t;
+    ranges_valid = true;
+    return 0;
+}
+
+int majorants(GridImpl* g, const DevTF& tf, cudaStream_t s, uint8_t* d_empty)
+{
+    int nc = g->cells[0] * g->cells[1] * g->cells[2];
+    k_majorants<<<(nc + 255) / 256, 256, sizeof(float4) * size_t(tf.n), s>>>(tf, g->d_tf, g->d_cmin, g->d_cmax, nc,
+                                                                            g->d_maj, d_empty);
+    SVDB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** out)
+{
+    *out = nullptr;
+    if (!b && n)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "svdb bytes are null");
+    if (codec < 0 || codec > SVDBGPU_CODEC_AUTO8)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "unknown codec");
+    // ---- parse_frozen validation (io.hpp:183-256) ----
+    if (n < 4)
+        return fail(Errc::corrupt_index, "unexpected end of SVDB data");
+    if (std::memcmp(b, "SVDB", 4) != 0)
+        return fail(Errc::bad_magic, "not an SVDB file");
+    if (n < 8)
+        return fail(Errc::corrupt_index, "unexpected end of SVDB data");
+    uint32_t version = rd_u32(b + 4);
+    if (version != 1)
+        return fail(Errc::version_mismatch, "unsupported SVDB version " + std::to_string(version));
+    if (n < kHdr)
+        return fail(Errc::corrupt_index, "unexpected end of SVDB data");
+    uint32_t vt = rd_u32(b + 8);
+    if (vt > 1)
+        return fail(Errc::corrupt_index, "invalid voxel type");
+    int dims[3] = {int(rd_u32(b + 12)), int(rd_u32(b + 16)), int(rd_u32(b + 20))};
+    if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
+        return fail(Errc::corrupt_index, "invalid dims");
+    uint64_t nu = rd_u64(b + 36), nl = rd_u64(b + 44), nf = rd_u64(b + 52), nr = rd_u64(b + 60);
+    const uint64_t lim = 1ull << 32;
+    if (nu > lim || nl > lim || nf > lim || nr > lim)
+        return fail(Errc::corrupt_index, "implausible section counts");
+    if (kHdr + kRootRec * nr + kUpperRec * nu + kLowerRec * nl + kLeafRec * nf != n)
+        return fail(Errc::corrupt_index, "section counts do not match data size");
+    const uint8_t* root = b + kHdr;
+    const uint8_t* up = root + kRootRec * nr;
+    const uint8_t* low = up + kUpperRec * nu;
+    const uint8_t* leaf = low + kLowerRec * nl;
+    std::vector<int4> h_root(size_t(nr ? nr : 1));
+    for (uint64_t i = 0; i < nr; ++i) {
+        const uint8_t* e = root + 16 * i;
+        h_root[i] = make_int4(rd_i32(e), rd_i32(e + 4), rd_i32(e + 8), int(rd_u32(e + 12)));
+        if (rd_u32(e + 12) >= nu)
+            return fail(Errc::corrupt_index, "root entry references missing upper node");
+    }
+    std::vector<uint2> h_upper(size_t(nu) * 32768);
+    for (uint64_t i = 0; i < nu; ++i) {
+        const uint8_t* r = up + kUpperRec * i;
+        const uint8_t* child = r + 16 + 4 * 32768;
+        const uint8_t* tile = child + 4096;
+        for (int s = 0; s < 32768; ++s) {
+            uint32_t p = rd_u32(r + 16 + 4 * s);
+            bool c = bit(child, s);
+            if (c && p >= nl)
+                return fail(Errc::corrupt_index, "upper node child index out of range");
+            h_upper[i * 32768 + s] = bit(tile, s) ? make_uint2(kSlotTile, p) : (c ? make_uint2(kSlotChild, p) : make_uint2(0, 0));
+        }
+    }
+    std::vector<uint2> h_lower(size_t(nl) * 4096);
+    for (uint64_t i = 0; i < nl; ++i) {
+        const uint8_t* r = low + kLowerRec * i;
+        const uint8_t* child = r + 16 + 4 * 4096;
+        const uint8_t* tile = child + 512;
+        for (int s = 0; s < 4096; ++s) {
+            uint32_t p = rd_u32(r + 16 + 4 * s);
+            bool c = bit(child, s);
+            if (c && p >= nf)
+                return fail(Errc::corrupt_index, "lower node child index out of range");
+            h_lower[i * 4096 + s] = bit(tile, s) ? make_uint2(kSlotTile, p) : (c ? make_uint2(kSlotChild, p) : make_uint2(0, 0));
+        }
+    }
+
+    int ndev = 0;
+    SVDB_CUDA(cudaGetDeviceCount(&ndev));
+    if (ndev < 1)
+        return fail_code(SVDBGPU_E_NO_DEVICE, "no CUDA device (no CPU fallback)");
+    if (device < 0 || device >= ndev)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "device ordinal out of range");
+    SVDB_CUDA(cudaSetDevice(device));
+
+    auto g = std::make_unique<GridImpl>();
+    g->device = device;
+    g->voxel_type = int(vt);
+    g->value_domain[0] = rd_f32(b + 28);
+    g->value_domain[1] = rd_f32(b + 32);
+    g->n_upper = nu;
+    g->n_lower = nl;
+    g->n_leaf = nf;
+    g->n_root = nr;
+    g->svdb_bytes = n;
+    SVDB_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    SVDB_CUDA(cudaEventCreate(&g->ev0));
+    SVDB_CUDA(cudaEventCreate(&g->ev1));
+    SVDB_CUDA(cudaMalloc(&g->d_counters, 64));
+    cudaStream_t s = g->stream;
+
+    SVDB_CUDA(cudaMalloc(&g->d_root, sizeof(int4) * h_root.size()));
+    SVDB_CUDA(cudaMemcpyAsync(g->d_root, h_root.data(), sizeof(int4) * h_root.size(), cudaMemcpyHostToDevice, s));
+    SVDB_CUDA(cudaMalloc(&g->d_upper, sizeof(uint2) * (h_upper.size() ? h_upper.size() : 1)));
+    if (!h_upper.empty())
+        SVDB_CUDA(cudaMemcpyAsync(g->d_upper, h_upper.data(), sizeof(uint2) * h_upper.size(), cudaMemcpyHostToDevice, s));
+    SVDB_CUDA(cudaMalloc(&g->d_lower, sizeof(uint4) * (h_lower.size() ? h_lower.size() : 1)));
+
+    // ---- leaves: stage records in chunks, encode with the codec ----
+    int resolved = codec;
+    if (codec == SVDBGPU_CODEC_AUTO8)
+        resolved = vt == 0 ? kCodecUnorm8 : kCodecAffine8;
+    const uint32_t stride = resolved == kCodecF32 ? 2048u : (resolved == kCodecAffine4 ? 256u : 512u);
+    float2* d_params = nullptr;
+    uint2* d_lstage = nullptr;
+    uint8_t* d_stage = nullptr;
+    int* d_bad = nullptr;
+    const uint64_t chunk = std::min<uint64_t>(nf ? nf : 1, 1ull << 18); // 256 Ki leaves = 558 MB staging
+    SVDB_CUDA(cudaMalloc(&d_params, sizeof(float2) * (nf ? nf : 1)));
+    SVDB_CUDA(cudaMalloc(&d_bad, sizeof(int)));
+    SVDB_CUDA(cudaMalloc(&g->d_codes, size_t(stride) * (nf ? nf : 1)));
+    if (nf)
+        SVDB_CUDA(cudaMalloc(&d_stage, size_t(kLeafRec * chunk)));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        SVDB_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+        for (uint64_t first = 0; first < nf; first += chunk) {
+            uint64_t cnt = std::min(chunk, nf - first);
+            SVDB_CUDA(cudaMemcpyAsync(d_stage, leaf + kLeafRec * first, size_t(kLeafRec * cnt), cudaMemcpyHostToDevice, s));
+            unsigned blocks = unsigned((cnt + 7) / 8);
+            uint8_t* dst = g->d_codes + size_t(stride) * first;
+            float2* par = d_params + first;
+#define LAUNCH_ENCODE(C) k_leaf_encode<C><<<blocks, 256, 0, s>>>(d_stage, cnt, dst, par, d_bad)
+            SVDB_CODEC_DISPATCH(resolved, LAUNCH_ENCODE)
+#undef LAUNCH_ENCODE
+            SVDB_CUDA(cudaGetLastError());
+        }
+        int bad = 0;
+        SVDB_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SVDB_CUDA(cudaStreamSynchronize(s));
+        if (!bad)
+            break;
+        if (codec == SVDBGPU_CODEC_AUTO8 && resolved == kCodecUnorm8) {
+            resolved = kCodecAffine8; // same stride
+            continue;
+        }
+        cudaFree(d_stage);
+        cudaFree(d_params);
+        cudaFree(d_bad);
+        return fail(Errc::size_mismatch, "UNORM8 codec needs every leaf value to be byte/255 exact");
+    }
+    cudaFree(d_stage);
+    cudaFree(d_bad);
+    if (nl) {
+        SVDB_CUDA(cudaMalloc(&d_lstage, sizeof(uint2) * h_lower.size()));
+        SVDB_CUDA(cudaMemcpyAsync(d_lstage, h_lower.data(), sizeof(uint2) * h_lower.size(), cudaMemcpyHostToDevice, s));
+        k_expand_lower<<<grid_blocks(h_lower.size()), 256, 0, s>>>(d_lstage, h_lower.size(), d_params, g->d_lower);
+        SVDB_CUDA(cudaGetLastError());
+    }
+    SVDB_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d_lstage);
+    cudaFree(d_params);
+
+    g->codec = resolved;
+    g->dg.dims[0] = dims[0];
+    g->dg.dims[1] = dims[1];
+    g->dg.dims[2] = dims[2];
+    g->dg.background = rd_f32(b + 24);
+    g->dg.n_root = int(nr);
+    g->dg.root = g->d_root;
+    g->dg.upper = g->d_upper;
+    g->dg.lower = g->d_lower;
+    g->dg.codes = g->d_codes;
+    g->dg.leaf_stride = stride;
+    g->leaf_payload_bytes = uint64_t(stride) * nf + 8 * nf;
+    g->device_bytes = sizeof(int4) * h_root.size() + sizeof(uint2) * h_upper.size() + sizeof(uint4) * h_lower.size() +
+                      uint64_t(stride) * nf;
+    *out = g.release();
+    return 0;
+}
+
+int grid_leaf_codes(const GridImpl* g, uint64_t first, uint64_t count, uint8_t* codes, float* params)
+{
+    if (first + count > g->n_leaf)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "leaf range out of bounds");
+    SVDB_CUDA(cudaSetDevice(g->device));
+    if (codes && count)
+        SVDB_CUDA(cudaMemcpy(codes, g->d_codes + size_t(g->dg.leaf_stride) * first,
+                             size_t(g->dg.leaf_stride) * count, cudaMemcpyDeviceToHost));
+    if (params && count) {
+        // params live folded in the lower table; recover them by scanning it on the host
+        std::vector<uint4> low(size_t(g->n_lower) * 4096);
+        SVDB_CUDA(cudaMemcpy(low.data(), g->d_lower, sizeof(uint4) * low.size(), cudaMemcpyDeviceToHost));
+        for (auto& e : low)
+            if (e.x == kSlotChild && e.y >= first && e.y < first + count) {
+                std::memcpy(&params[2 * (e.y - first)], &e.z, 4);
+                std::memcpy(&params[2 * (e.y - first) + 1], &e.w, 4);
+            }
+    }
+    return 0;
+}
+
+int read_voxels_device(const GridImpl* g, const int32_t* d_ijk, size_t n, float* d_out, cudaStream_t s)
+{
+    if (!n)
+        return 0;
+#define LAUNCH_RV(C) k_read_voxels<C><<<grid_blocks(n), 256, 0, s>>>(g->dg, d_ijk, n, d_out)
+    SVDB_CODEC_DISPATCH(g->codec, LAUNCH_RV)
+#undef LAUNCH_RV
+    SVDB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int sample_device(const GridImpl* g, const double* d_xyz, size_t n, int mode, float* d_out, cudaStream_t s)
+{
+    if (!n)
+        return 0;
+#define LAUNCH_S(C) k_sample<C><<<grid_blocks(n), 256, 0, s>>>(g->dg, d_xyz, n, mode, d_out)
+    SVDB_CODEC_DISPATCH(g->codec, LAUNCH_S)
+#undef LAUNCH_S
+    SVDB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int gradient_device(const GridImpl* g, const double* d_xyz, size_t n, double* d_out, cudaStream_t s)
+{
+    if (!n)
+        return 0;
+#define LAUNCH_G(C) k_gradient<C><<<grid_blocks(n), 256, 0, s>>>(g->dg, d_xyz, n, d_out)
+    SVDB_CODEC_DISPATCH(g->codec, LAUNCH_G)
+#undef LAUNCH_G
+    SVDB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+} // namespace svdbgpu

@@ -1,0 +1,646 @@
+// host_encoder.cpp — native host side of the grid build: the fixed-rate encoder and the
+// synthetic-volume generators.
+//
+// svdbgpu_compress() produces the SVDB v1 container (io.hpp:22-43) BYTE-IDENTICAL to the
+// reference's serialize_frozen(compress(v, params).first) (compress.hpp:221-283,
+// frozen.hpp:136-218). The reference builds a pointer tree (SparseGridBuilder, tree.hpp:166)
+// and snapshots it; here the same decisions are made directly on dense per-level state
+// arrays, in parallel, and the container is written in one pass:
+//
+//   1. min/max + finite check          DenseVolume::from_data   volume.hpp:39-63
+//   2. histogram + exact mode          compute_histogram / detect_background volume.hpp:177-222
+//   3. brick scores, total order       build_brick_records      compress.hpp:114-145
+//   4. budget ceil(q * n) bricks       compress                 compress.hpp:237-251
+//   5. per-8^3-block leaf decision     activate_brick + corners compress.hpp:171-215, 253-268
+//   6. prune (uniform leaves -> tiles, uniform lowers -> upper tiles) tree.hpp:332-426
+//   7. z,y,x-ordered indices + write   freeze / write_frozen    frozen.hpp:136-218, io.hpp:121-165
+#include "svdbgpu.h"
+#include "svdbgpu_internal.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+namespace svdbgpu {
+
+int resolve_threads(int threads)
+{
+    if (threads > 0)
+        return threads;
+    unsigned n = std::thread::hardware_concurrency();
+    return n ? int(n) : 1;
+}
+
+void parallel_for(int64_t n, int threads, const std::function<void(int64_t, int64_t, int)>& body)
+{
+    int nt = int(std::min<int64_t>(resolve_threads(threads), std::max<int64_t>(n, 1)));
+    if (nt <= 1) {
+        body(0, n, 0);
+        return;
+    }
+    std::atomic<int64_t> next{0};
+    const int64_t chunk = std::max<int64_t>(1, n / (int64_t(nt) * 16));
+    std::vector<std::thread> pool;
+    pool.reserve(size_t(nt));
+    for (int t = 0; t < nt; ++t)
+        pool.emplace_back([&, t] {
+            for (;;) {
+                int64_t b = next.fetch_add(chunk);
+                if (b >= n)
+                    break;
+                body(b, std::min(n, b + chunk), t);
+            }
+        });
+    for (auto& th : pool)
+        th.join();
+}
+
+namespace {
+
+constexpr int kBrick = 32;
+constexpr uint64_t kHdr = 72, kRootRec = 16;
+constexpr uint64_t kUpperRec = 16 + 4ull * 32768 + 2ull * 4096;
+constexpr uint64_t kLowerRec = 16 + 4ull * 4096 + 2ull * 512;
+constexpr uint64_t kLeafRec = 16 + 64 + 4ull * 512;
+
+inline float nz(float v) { return v == 0.0f ? 0.0f : v; } // from_data's -0 normalisation
+
+struct Vol {
+    const float* p;
+    int dx, dy, dz;
+    float at(int x, int y, int z) const
+    {
+        return nz(p[size_t(x) + size_t(dx) * (size_t(y) + size_t(dy) * size_t(z))]);
+    }
+    const float* row(int x, int y, int z) const
+    {
+        return p + size_t(x) + size_t(dx) * (size_t(y) + size_t(dy) * size_t(z));
+    }
+};
+
+// similarity() (compress.hpp:56-66)
+double similarity(float lo, float hi, float bg, int metric)
+{
+    double dlo = std::abs(double(lo) - double(bg));
+    double dhi = std::abs(double(hi) - double(bg));
+    switch (metric) {
+    case 0: return std::min(dlo, dhi);
+    case 1: return std::max(dlo, dhi);
+    default: return std::abs((double(lo) + double(hi)) * 0.5 - double(bg));
+    }
+}
+
+struct Brick {
+    float lo, hi;
+    double score;
+    uint64_t index;
+};
+
+enum : uint8_t { kAbsent = 0, kLeaf = 1, kTile = 2, kCornerLeaf = 3 }; // kCornerLeaf: only set_voxel'd corners active
+
+inline void put_u32(uint8_t* p, uint32_t v) { std::memcpy(p, &v, 4); }
+inline void put_i32(uint8_t* p, int32_t v) { std::memcpy(p, &v, 4); }
+inline void put_u64(uint8_t* p, uint64_t v) { std::memcpy(p, &v, 8); }
+inline void put_f32(uint8_t* p, float v) { std::memcpy(p, &v, 4); }
+inline void set_bit(uint8_t* words, int i) { words[i >> 3] |= uint8_t(1u << (i & 7)); }
+inline uint32_t f32_bits(float f) { uint32_t u; std::memcpy(&u, &f, 4); return u; }
+
+} // namespace
+
+int compress(const float* data, const int32_t dims[3], int voxel_type, double quality, int metric,
+             int threads, std::vector<uint8_t>& out, svdbgpu_compress_report* rep)
+{
+    if (!(quality >= 0.0 && quality <= 1.0))
+        return fail(Errc::invalid_quality, "quality must be in [0,1]");
+    if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
+        return fail(Errc::size_mismatch, "volume dims must be positive");
+    if (voxel_type != 0 && voxel_type != 1)
+        return fail(Errc::size_mismatch, "voxel_type must be 0 (u8) or 1 (f32)");
+    const Vol v{data, dims[0], dims[1], dims[2]};
+    const int64_t nvox = int64_t(dims[0]) * dims[1] * dims[2];
+    const int nt = resolve_threads(threads);
+    const int64_t rows = int64_t(dims[1]) * dims[2];
+
+    // 1. min / max / finiteness (volume.hpp:41-62)
+    std::vector<float> tmin(size_t(nt), std::numeric_limits<float>::infinity());
+    std::vector<float> tmax(size_t(nt), -std::numeric_limits<float>::infinity());
+    std::atomic<bool> nonfinite{false};
+    parallel_for(rows, nt, [&](int64_t b, int64_t e, int t) {
+        float mn = tmin[size_t(t)], mx = tmax[size_t(t)];
+        for (int64_t r = b; r < e; ++r) {
+            const float* row = data + size_t(r) * size_t(dims[0]);
+            for (int x = 0; x < dims[0]; ++x) {
+                float s = nz(row[x]);
+                if (!std::isfinite(s))
+                    nonfinite = true;
+                mn = std::min(mn, s);
+                mx = std::max(mx, s);
+            }
+        }
+        tmin[size_t(t)] = mn;
+        tmax[size_t(t)] = mx;
+    });
+    if (nonfinite)
+        return fail(Errc::non_finite_voxel, "volume contains NaN or Inf");
+    float vmin = std::numeric_limits<float>::infinity(), vmax = -vmin;
+    for (int t = 0; t < nt; ++t) {
+        vmin = std::min(vmin, tmin[size_t(t)]);
+        vmax = std::max(vmax, tmax[size_t(t)]);
+    }
+
+    // 2. histogram + background (volume.hpp:177-222)
+    const int bins = voxel_type == 0 ? 256 : 1024;
+    const double hlo = vmin, hhi = vmax;
+    auto bin_of = [&](double s) {
+        if (hhi <= hlo)
+            return 0;
+        int b = int(std::floor((s - hlo) / (hhi - hlo) * double(bins)));
+        return std::clamp(b, 0, bins - 1);
+    };
+    std::vector<std::vector<uint64_t>> th(size_t(nt), std::vector<uint64_t>(size_t(bins), 0));
+    parallel_for(rows, nt, [&](int64_t b, int64_t e, int t) {
+        auto& h = th[size_t(t)];
+        for (int64_t r = b; r < e; ++r) {
+            const float* row = data + size_t(r) * size_t(dims[0]);
+            for (int x = 0; x < dims[0]; ++x)
+                ++h[size_t(bin_of(nz(row[x])))];
+        }
+    });
+    std::vector<uint64_t> hist(size_t(bins), 0);
+    for (auto& h : th)
+        for (int i = 0; i < bins; ++i)
+            hist[size_t(i)] += h[size_t(i)];
+    int best_bin = 0;
+    for (int i = 1; i < bins; ++i)
+        if (hist[size_t(i)] > hist[size_t(best_bin)])
+            best_bin = i;
+    std::vector<std::unordered_map<float, uint64_t>> exact(static_cast<size_t>(nt));
+    parallel_for(rows, nt, [&](int64_t b, int64_t e, int t) {
+        auto& m = exact[size_t(t)];
+        for (int64_t r = b; r < e; ++r) {
+            const float* row = data + size_t(r) * size_t(dims[0]);
+            for (int x = 0; x < dims[0]; ++x) {
+                float s = nz(row[x]);
+                if (bin_of(s) == best_bin)
+                    ++m[s];
+            }
+        }
+    });
+    for (int t = 1; t < nt; ++t)
+        for (auto& [val, cnt] : exact[size_t(t)])
+            exact[0][val] += cnt;
+    bool have = false;
+    float bg = 0.0f;
+    uint64_t best_count = 0;
+    for (auto& [val, cnt] : exact[0])
+        if (!have || cnt > best_count || (cnt == best_count && val < bg)) {
+            have = true;
+            bg = val;
+            best_count = cnt;
+        }
+
+    // 3. brick records + total order (compress.hpp:97-145)
+    const int nbx = (dims[0] + kBrick - 1) / kBrick, nby = (dims[1] + kBrick - 1) / kBrick,
+              nbz = (dims[2] + kBrick - 1) / kBrick;
+    const int64_t total = int64_t(nbx) * nby * nbz;
+    std::vector<Brick> bricks(static_cast<size_t>(total));
+    parallel_for(total, nt, [&](int64_t b, int64_t e, int) {
+        for (int64_t i = b; i < e; ++i) {
+            int bx = int(i % nbx), by = int((i / nbx) % nby), bz = int(i / (int64_t(nbx) * nby));
+            int x0 = bx * kBrick, y0 = by * kBrick, z0 = bz * kBrick;
+            int x1 = std::min(x0 + kBrick, dims[0]), y1 = std::min(y0 + kBrick, dims[1]),
+                z1 = std::min(z0 + kBrick, dims[2]);
+            float mn = std::numeric_limits<float>::infinity(), mx = -mn;
+            for (int z = z0; z < z1; ++z)
+                for (int y = y0; y < y1; ++y) {
+                    const float* row = v.row(x0, y, z);
+                    for (int x = 0; x < x1 - x0; ++x) {
+                        float s = nz(row[x]);
+                        mn = std::min(mn, s);
+                        mx = std::max(mx, s);
+                    }
+                }
+            bricks[size_t(i)] = {mn, mx, similarity(mn, mx, bg, metric), uint64_t(i)};
+        }
+    });
+    std::sort(bricks.begin(), bricks.end(), [bg](const Brick& a, const Brick& b) {
+        if (a.score != b.score)
+            return a.score > b.score;
+        bool abg = a.lo == bg && a.hi == bg, bbg = b.lo == bg && b.hi == bg;
+        if (abg != bbg)
+            return !abg;
+        return a.index < b.index;
+    });
+    const uint64_t budget =
+        std::min<uint64_t>(uint64_t(total), uint64_t(std::ceil(quality * double(total))));
+    std::vector<uint8_t> chosen(size_t(total), 0);
+    uint64_t voxels_activated = 0;
+    for (uint64_t i = 0; i < budget; ++i) {
+        uint64_t idx = bricks[size_t(i)].index;
+        chosen[size_t(idx)] = 1;
+        int bx = int(idx % nbx), by = int((idx / nbx) % nby), bz = int(idx / (uint64_t(nbx) * nby));
+        uint64_t ex = uint64_t(std::min(kBrick, dims[0] - bx * kBrick)),
+                 ey = uint64_t(std::min(kBrick, dims[1] - by * kBrick)),
+                 ez = uint64_t(std::min(kBrick, dims[2] - bz * kBrick));
+        voxels_activated += ex * ey * ez;
+    }
+    const int cx1 = dims[0] - 1, cy1 = dims[1] - 1, cz1 = dims[2] - 1;
+    auto brick_of = [&](int x, int y, int z) {
+        return size_t(x / kBrick) + size_t(nbx) * (size_t(y / kBrick) + size_t(nby) * size_t(z / kBrick));
+    };
+    if (!chosen[brick_of(0, 0, 0)])
+        ++voxels_activated;
+    if ((cx1 | cy1 | cz1) != 0 && !chosen[brick_of(cx1, cy1, cz1)])
+        ++voxels_activated;
+
+    // 5 + 6a. per-leaf-block decision (activate_brick, corners, leaf-level prune)
+    const int lx = (dims[0] + 7) / 8, ly = (dims[1] + 7) / 8, lz = (dims[2] + 7) / 8;
+    const int64_t nblk = int64_t(lx) * ly * lz;
+    std::vector<uint8_t> state(size_t(nblk), kAbsent);
+    std::vector<float> tile_val(size_t(nblk), 0.0f);
+    auto is_corner_block = [&](int bx, int by, int bz) {
+        return (bx == 0 && by == 0 && bz == 0) || (bx == cx1 / 8 && by == cy1 / 8 && bz == cz1 / 8);
+    };
+    parallel_for(nblk, nt, [&](int64_t b, int64_t e, int) {
+        for (int64_t i = b; i < e; ++i) {
+            int bx = int(i % lx), by = int((i / lx) % ly), bz = int(i / (int64_t(lx) * ly));
+            int x0 = bx * 8, y0 = by * 8, z0 = bz * 8;
+            bool corner = is_corner_block(bx, by, bz);
+            uint8_t st = kAbsent;
+            if (chosen[brick_of(x0, y0, z0)]) {
+                bool full = x0 + 8 <= dims[0] && y0 + 8 <= dims[1] && z0 + 8 <= dims[2];
+                if (!full) {
+                    st = kLeaf; // set_voxel path: partially active, never collapses
+                } else {
+                    bool all_bg = true, uniform = true;
+                    float v0 = v.at(x0, y0, z0);
+                    for (int z = 0; z < 8; ++z)
+                        for (int y = 0; y < 8; ++y) {
+                            const float* row = v.row(x0, y0 + y, z0 + z);
+                            for (int x = 0; x < 8; ++x) {
+                                float s = nz(row[x]);
+                                all_bg &= !(s != bg);
+                                uniform &= !(s != v0);
+                            }
+                        }
+                    if (!all_bg) {
+                        if (uniform) {
+                            st = kTile; // fully active uniform leaf -> lower tile (v0 != B)
+                            tile_val[size_t(i)] = v0;
+                        } else {
+                            st = kLeaf;
+                        }
+                    }
+                }
+            }
+            if (corner && st == kAbsent)
+                st = kCornerLeaf; // corner set_voxel creates a background leaf, partially active
+            state[size_t(i)] = st;
+        }
+    });
+
+    // 6b. lower-level prune: lower regions (128^3) collapse / vanish (tree.hpp:338-375)
+    const int wx = (dims[0] + 127) / 128, wy = (dims[1] + 127) / 128, wz = (dims[2] + 127) / 128;
+    const int64_t nlow = int64_t(wx) * wy * wz;
+    // lower state: 0 absent, 1 kept, 2 collapsed to an upper tile
+    std::vector<uint8_t> lstate(size_t(nlow), 0);
+    std::vector<float> ltile(size_t(nlow), 0.0f);
+    parallel_for(nlow, nt, [&](int64_t b, int64_t e, int) {
+        for (int64_t i = b; i < e; ++i) {
+            int ox = int(i % wx) * 16, oy = int((i / wx) % wy) * 16, oz = int(i / (int64_t(wx) * wy)) * 16;
+            bool any_leaf = false, any_tile = false, all_tiles = true, same = true, first = true;
+            float tv = 0.0f;
+            for (int z = oz; z < oz + 16; ++z)
+                for (int y = oy; y < oy + 16; ++y)
+                    for (int x = ox; x < ox + 16; ++x) {
+                        uint8_t st = kAbsent;
+                        float val = 0.0f;
+                        if (x < lx && y < ly && z < lz) {
+                            size_t k = size_t(x) + size_t(lx) * (size_t(y) + size_t(ly) * size_t(z));
+                            st = state[k];
+                            val = tile_val[k];
+                        }
+                        any_leaf |= st == kLeaf || st == kCornerLeaf;
+                        if (st == kTile) {
+                            any_tile = true;
+                            if (first) {
+                                tv = val;
+                                first = false;
+                            } else if (val != tv) {
+                                same = false;
+                            }
+                        } else {
+                            all_tiles = false;
+                        }
+                    }
+            if (any_leaf)
+                lstate[size_t(i)] = 1;
+            else if (all_tiles && same && !first) {
+                lstate[size_t(i)] = 2;
+                ltile[size_t(i)] = tv;
+            } else if (any_tile)
+                lstate[size_t(i)] = 1;
+            else
+                lstate[size_t(i)] = 0;
+        }
+    });
+
+    // 7. indices in (z,y,x) origin order (frozen.hpp:144-173)
+    std::vector<uint32_t> leaf_index(size_t(nblk), 0);
+    uint64_t n_leaf = 0;
+    for (int64_t i = 0; i < nblk; ++i)
+        if (state[size_t(i)] == kLeaf || state[size_t(i)] == kCornerLeaf) {
+            // blocks inside a removed lower cannot exist: a lower with a leaf is kept
+            leaf_index[size_t(i)] = uint32_t(n_leaf++);
+        }
+    std::vector<uint32_t> lower_index(size_t(nlow), 0);
+    uint64_t n_lower = 0;
+    for (int64_t i = 0; i < nlow; ++i)
+        if (lstate[size_t(i)] == 1)
+            lower_index[size_t(i)] = uint32_t(n_lower++);
+    const int ux = (dims[0] + 4095) / 4096, uy = (dims[1] + 4095) / 4096, uz = (dims[2] + 4095) / 4096;
+    const int64_t nup = int64_t(ux) * uy * uz;
+    std::vector<int64_t> upper_index(size_t(nup), -1);
+    uint64_t n_upper = 0;
+    for (int64_t u = 0; u < nup; ++u) {
+        int ox = int(u % ux) * 32, oy = int((u / ux) % uy) * 32, oz = int(u / (int64_t(ux) * uy)) * 32;
+        bool any = false;
+        for (int z = oz; z < std::min(oz + 32, wz) && !any; ++z)
+            for (int y = oy; y < std::min(oy + 32, wy) && !any; ++y)
+                for (int x = ox; x < std::min(ox + 32, wx) && !any; ++x)
+                    any = lstate[size_t(x) + size_t(wx) * (size_t(y) + size_t(wy) * size_t(z))] != 0;
+        if (any)
+            upper_index[size_t(u)] = int64_t(n_upper++);
+    }
+
+    const uint64_t total_bytes =
+        kHdr + kRootRec * n_upper + kUpperRec * n_upper + kLowerRec * n_lower + kLeafRec * n_leaf;
+    out.assign(size_t(total_bytes), 0);
+    uint8_t* o = out.data();
+    // header (io.hpp:124-137)
+    std::memcpy(o, "SVDB", 4);
+    put_u32(o + 4, 1);
+    put_u32(o + 8, uint32_t(voxel_type));
+    put_u32(o + 12, uint32_t(dims[0]));
+    put_u32(o + 16, uint32_t(dims[1]));
+    put_u32(o + 20, uint32_t(dims[2]));
+    put_f32(o + 24, bg);
+    put_f32(o + 28, vmin);
+    put_f32(o + 32, vmax);
+    put_u64(o + 36, n_upper);
+    put_u64(o + 44, n_lower);
+    put_u64(o + 52, n_leaf);
+    put_u64(o + 60, n_upper);
+    uint8_t* root = o + kHdr;
+    uint8_t* up = root + kRootRec * n_upper;
+    uint8_t* low = up + kUpperRec * n_upper;
+    uint8_t* leaf = low + kLowerRec * n_lower;
+
+    for (int64_t u = 0; u < nup; ++u) {
+        if (upper_index[size_t(u)] < 0)
+            continue;
+        uint64_t ui = uint64_t(upper_index[size_t(u)]);
+        int ox = int(u % ux) * 32, oy = int((u / ux) % uy) * 32, oz = int(u / (int64_t(ux) * uy)) * 32;
+        uint8_t* e = root + kRootRec * ui;
+        put_i32(e, ox * 128);
+        put_i32(e + 4, oy * 128);
+        put_i32(e + 8, oz * 128);
+        put_u32(e + 12, uint32_t(ui));
+        uint8_t* r = up + kUpperRec * ui;
+        put_i32(r, ox * 128);
+        put_i32(r + 4, oy * 128);
+        put_i32(r + 8, oz * 128);
+        uint8_t* child = r + 16 + 4 * 32768;
+        uint8_t* tile = child + 4096;
+        for (int z = oz; z < std::min(oz + 32, wz); ++z)
+            for (int y = oy; y < std::min(oy + 32, wy); ++y)
+                for (int x = ox; x < std::min(ox + 32, wx); ++x) {
+                    size_t li = size_t(x) + size_t(wx) * (size_t(y) + size_t(wy) * size_t(z));
+                    int slot = (x - ox) + 32 * ((y - oy) + 32 * (z - oz));
+                    if (lstate[li] == 1) {
+                        set_bit(child, slot);
+                        put_u32(r + 16 + 4 * slot, lower_index[li]);
+                    } else if (lstate[li] == 2) {
+                        set_bit(tile, slot);
+                        put_u32(r + 16 + 4 * slot, f32_bits(ltile[li]));
+                    }
+                }
+    }
+    parallel_for(nlow, nt, [&](int64_t b, int64_t e, int) {
+        for (int64_t i = b; i < e; ++i) {
+            if (lstate[size_t(i)] != 1)
+                continue;
+            int ox = int(i % wx) * 16, oy = int((i / wx) % wy) * 16, oz = int(i / (int64_t(wx) * wy)) * 16;
+            uint8_t* r = low + kLowerRec * lower_index[size_t(i)];
+            put_i32(r, ox * 8);
+            put_i32(r + 4, oy * 8);
+            put_i32(r + 8, oz * 8);
+            uint8_t* child = r + 16 + 4 * 4096;
+            uint8_t* tile = child + 512;
+            for (int z = oz; z < std::min(oz + 16, lz); ++z)
+                for (int y = oy; y < std::min(oy + 16, ly); ++y)
+                    for (int x = ox; x < std::min(ox + 16, lx); ++x) {
+                        size_t k = size_t(x) + size_t(lx) * (size_t(y) + size_t(ly) * size_t(z));
+                        int slot = (x - ox) + 16 * ((y - oy) + 16 * (z - oz));
+                        if (state[k] == kLeaf || state[k] == kCornerLeaf) {
+                            set_bit(child, slot);
+                            put_u32(r + 16 + 4 * slot, leaf_index[k]);
+                        } else if (state[k] == kTile) {
+                            set_bit(tile, slot);
+                            put_u32(r + 16 + 4 * slot, f32_bits(tile_val[k]));
+                        }
+                    }
+        }
+    });
+    parallel_for(nblk, nt, [&](int64_t b, int64_t e, int) {
+        for (int64_t i = b; i < e; ++i) {
+            if (state[size_t(i)] != kLeaf && state[size_t(i)] != kCornerLeaf)
+                continue;
+            int bx = int(i % lx), by = int((i / lx) % ly), bz = int(i / (int64_t(lx) * ly));
+            int x0 = bx * 8, y0 = by * 8, z0 = bz * 8;
+            uint8_t* r = leaf + kLeafRec * leaf_index[size_t(i)];
+            put_i32(r, x0);
+            put_i32(r + 4, y0);
+            put_i32(r + 8, z0);
+            uint8_t* mask = r + 16;
+            float* vals = reinterpret_cast<float*>(r + 80); // 16-aligned inside the record
+            bool brick = state[size_t(i)] == kLeaf; // activated by its brick (not corner-only)
+            for (int z = 0; z < 8; ++z)
+                for (int y = 0; y < 8; ++y)
+                    for (int x = 0; x < 8; ++x) {
+                        int gx = x0 + x, gy = y0 + y, gz = z0 + z;
+                        int vi = x + 8 * (y + 8 * z);
+                        bool inside = gx < dims[0] && gy < dims[1] && gz < dims[2];
+                        float val = bg;
+                        if (brick && inside) {
+                            val = v.at(gx, gy, gz);
+                            set_bit(mask, vi);
+                        }
+                        std::memcpy(&vals[vi], &val, 4);
+                    }
+            // corners (compress.hpp:253-263): set_voxel on (0,0,0) and dims-1
+            if (bx == 0 && by == 0 && bz == 0) {
+                float c = v.at(0, 0, 0);
+                std::memcpy(&vals[0], &c, 4);
+                set_bit(mask, 0);
+            }
+            if (bx == cx1 / 8 && by == cy1 / 8 && bz == cz1 / 8) {
+                int vi = (cx1 & 7) + 8 * ((cy1 & 7) + 8 * (cz1 & 7));
+                float c = v.at(cx1, cy1, cz1);
+                std::memcpy(&vals[vi], &c, 4);
+                set_bit(mask, vi);
+            }
+        }
+    });
+
+    if (rep) {
+        rep->background = bg;
+        rep->num_bricks = uint64_t(total);
+        rep->bricks_activated = budget;
+        rep->voxels_activated = voxels_activated;
+        rep->frozen_bytes = total_bytes;
+        rep->dense_bytes = uint64_t(nvox) * 4;
+        rep->achieved_ratio = double(total_bytes) / double(rep->dense_bytes);
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Synthetic volumes (BASELINE.json configs). Deterministic from the seed; the
+// lattice of every value-noise octave is hashed with splitmix64 (rng.hpp:12-24 semantics).
+namespace {
+
+uint64_t mix64(uint64_t x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+uint64_t hash_counter(uint64_t seed, uint64_t c) { return mix64(mix64(seed) ^ c); }
+
+// One value-noise octave: lattice of (cells+2)^3 values in [-1,1], smoothstep-interpolated.
+// Rows are evaluated separably: the (y,z) bilinear blend of the lattice is done once per x-row,
+// leaving one 1-D smoothstep lerp per voxel.
+struct Octave {
+    int cells, n;
+    double scale; // lattice units per voxel
+    std::vector<float> lat;
+    Octave(int cells_, int dim_max, uint64_t seed) : cells(cells_)
+    {
+        n = cells + 2;
+        scale = double(cells) / double(std::max(1, dim_max - 1));
+        lat.resize(size_t(n) * n * n);
+        for (size_t i = 0; i < lat.size(); ++i)
+            lat[i] = float(double(hash_counter(seed, i) >> 11) * 0x1.0p-53 * 2.0 - 1.0);
+    }
+    static double smooth(double f) { return f * f * (3.0 - 2.0 * f); }
+    // row[i] = lattice blended at (y, z) for every lattice x index i
+    void row(int y, int z, double* out) const
+    {
+        double v = y * scale, w = z * scale;
+        int j = std::min(int(v), cells), k = std::min(int(w), cells);
+        double fv = smooth(v - j), fw = smooth(w - k);
+        const float* p00 = &lat[size_t(n) * (size_t(j) + size_t(n) * size_t(k))];
+        const float* p10 = p00 + n;
+        const float* p01 = p00 + size_t(n) * n;
+        const float* p11 = p01 + n;
+        for (int i = 0; i < n; ++i) {
+            double a = p00[i] + (p10[i] - double(p00[i])) * fv;
+            double b = p01[i] + (p11[i] - double(p01[i])) * fv;
+            out[i] = a + (b - a) * fw;
+        }
+    }
+    double at_x(const double* r, int x) const
+    {
+        double u = x * scale;
+        int i = std::min(int(u), cells);
+        return r[i] + (r[i + 1] - r[i]) * smooth(u - i);
+    }
+};
+
+inline float quantise_u8(double v)
+{
+    double c = std::clamp(v, 0.0, 1.0);
+    int b = int(std::lround(c * 255.0));
+    return float(b) / 255.0f; // load_raw's u8 mapping (volume.hpp:97)
+}
+
+} // namespace
+
+int synth(int kind, const int32_t dims[3], uint64_t seed, int threads, float* out)
+{
+    if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
+        return fail(Errc::size_mismatch, "synth dims must be positive");
+    const int dmax = std::max(dims[0], std::max(dims[1], dims[2]));
+    const int64_t rows = int64_t(dims[1]) * dims[2];
+    std::vector<Octave> oct;
+    int octaves = kind == 0 ? 0 : (kind == 2 ? 6 : 5);
+    int base_cells = kind == 2 ? 4 : 6;
+    for (int o = 0; o < octaves; ++o)
+        oct.emplace_back(base_cells << o, dmax, seed * 1315423911ull + uint64_t(o) + 1);
+    const double cx = 0.5 * (dims[0] - 1), cy = 0.5 * (dims[1] - 1), cz = 0.5 * (dims[2] - 1);
+    const double pi = 3.14159265358979323846;
+    parallel_for(rows, threads, [&](int64_t b, int64_t e, int) {
+        std::vector<double> lrow;
+        std::vector<const double*> rp(static_cast<size_t>(octaves));
+        for (int o = 0; o < octaves; ++o)
+            lrow.resize(lrow.size() + size_t(oct[size_t(o)].n));
+        for (int64_t r = b; r < e; ++r) {
+            int y = int(r % dims[1]), z = int(r / dims[1]);
+            float* row = out + size_t(r) * size_t(dims[0]);
+            size_t off = 0;
+            for (int o = 0; o < octaves; ++o) {
+                oct[size_t(o)].row(y, z, lrow.data() + off);
+                rp[size_t(o)] = lrow.data() + off;
+                off += size_t(oct[size_t(o)].n);
+            }
+            for (int x = 0; x < dims[0]; ++x) {
+                double val = 0.0;
+                if (kind == 0) {
+                    // Marschner-Lobb (f_M = 6, alpha = 0.25) on [-1,1]^3
+                    auto m = [](int i, int d) { return d > 1 ? -1.0 + 2.0 * double(i) / double(d - 1) : 0.0; };
+                    double px = m(x, dims[0]), py = m(y, dims[1]), pz = m(z, dims[2]);
+                    const double fm = 6.0, a = 0.25;
+                    double rr = std::sqrt(px * px + py * py);
+                    double rho_r = std::cos(2.0 * pi * fm * std::cos(pi * rr / 2.0));
+                    val = (1.0 - std::sin(pi * pz / 2.0) + a * (1.0 + rho_r)) / (2.0 * (1.0 + a));
+                    row[x] = quantise_u8(val);
+                    continue;
+                }
+                double f = 0.0, amp = 1.0, norm = 0.0;
+                for (int o = 0; o < octaves; ++o) {
+                    double nv = oct[size_t(o)].at_x(rp[size_t(o)], x);
+                    f += amp * (kind == 2 ? std::abs(nv) : nv);
+                    norm += amp;
+                    amp *= 0.5;
+                }
+                f /= norm;
+                if (kind == 1) {
+                    // fBm smoke: radial falloff, thresholded so the background is exactly 0
+                    double dx = (x - cx) / (0.5 * dims[0]), dy = (y - cy) / (0.5 * dims[1]),
+                           dz = (z - cz) / (0.5 * dims[2]);
+                    double fall = std::clamp(1.0 - std::sqrt(dx * dx + dy * dy + dz * dz), 0.0, 1.0);
+                    double d = (0.5 + 0.5 * f) * (0.35 + 0.65 * fall) - 0.25;
+                    row[x] = quantise_u8(d * 3.0);
+                } else if (kind == 2) {
+                    // ridged turbulence: 1 - |fBm| sharpened, dense f32 in [0,1]
+                    double t = 1.0 - f;
+                    row[x] = float(std::clamp(t * t * t, 0.0, 1.0));
+                } else {
+                    // sparse field: thresholded fBm, background exactly 0
+                    double d = 0.5 + 0.5 * f;
+                    row[x] = float(std::clamp((d - 0.60) * 4.0, 0.0, 1.0));
+                }
+            }
+        }
+    });
+    return 0;
+}
+
+} // namespace svdbgpu

@@ -1,0 +1,35 @@
+// layout.hpp — plain device-layout structs shared by host (C++) and device (CUDA) code.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace svdbgpu {
+
+enum SlotKind : uint32_t { kSlotBackground = 0, kSlotTile = 1, kSlotChild = 2 };
+
+// Device tree. Node tables are pre-resolved at upload so one load answers "what is in this
+// slot" with the reference's precedence (tile bit before child bit, frozen.hpp:88-97):
+//   upper: uint2 {kind, payload}         payload = lower index | f32 tile bits
+//   lower: uint4 {kind, payload, lo, sc} payload = leaf index | f32 tile bits; lo/sc = the
+//          child leaf's decode parameters, so a leaf miss costs one 16-B load + the codes.
+// Leaf payloads are one contiguous array, leaf i at codes + i * leaf_stride.
+struct DevGrid {
+    int dims[3];
+    float background;
+    int n_root;
+    const int4* root; // {origin x, y, z, upper index}, file order (z,y,x sorted)
+    const uint2* upper;
+    const uint4* lower;
+    const uint8_t* codes;
+    uint32_t leaf_stride; // bytes per leaf: 2048 f32, 512 u8, 256 u4
+};
+
+struct DevTF {
+    double lo, hi, scale;
+    int n;
+};
+
+constexpr int kCodecF32 = 0, kCodecUnorm8 = 1, kCodecAffine8 = 2, kCodecAffine4 = 3;
+
+} // namespace svdbgpu

@@ -1,0 +1,627 @@
+// render.cu — the path-tracing megakernel (K4) and the north-star integrators (K5 EA, K6 ratio),
+// plus the ISO marcher. One thread per pixel; each CTA is one 16x16 image tile (the reference's
+// tile, render.hpp:285-313), each warp an 8x4 pixel block so primary rays stay coherent.
+// Samples of a pixel run in index order and accumulate in FP64 (render.hpp:297-310), so the
+// image is independent of the launch shape and of how tiles are split across ranks/GPUs.
+//
+//   render_field  render.hpp:276-315   -> k_render
+//   camera_ray    render.hpp:259-269   -> host basis (exact) + camera_dir
+//   trace_path    render.hpp:160-187   -> trace_path
+//   next_event    render.hpp:137-151   -> next_event
+//   woodcock_track render.hpp:106-124  -> woodcock
+//   trace_iso     render.hpp:193-255   -> trace_iso
+#include "device.cuh"
+#include "grid_impl.hpp"
+
+#include <cmath>
+#include <cstring>
+
+namespace svdbgpu {
+
+namespace {
+
+struct CamArgs {
+    double pos[3], fwd[3], right[3], up[3];
+    double tan_half, aspect;
+    int w, h;
+};
+
+struct RenderArgs {
+    DevGrid g;
+    DevTF tf;
+    const float4* tf_ent;
+    const float* maj;
+    const float* cmin;
+    const float* cmax;
+    int cells[3];
+    double hi[3];
+    CamArgs cam;
+    int spp, max_bounces, rr_start;
+    uint64_t seed_mixed;
+    double iso;
+    float ambient[3], background[3];
+    double ea_step, ea_min_t;
+    int rank, nranks, tiles_x;
+    float* out;
+    int packed;
+    unsigned long long* counters;
+};
+
+constexpr double kPi = 3.14159265358979323846;
+
+__device__ __forceinline__ double kInf() { return __longlong_as_double(0x7ff0000000000000ll); }
+
+template <int CODEC>
+struct Tracer {
+    const RenderArgs& A;
+    const float4* ent; // shared-memory TF entries
+    Accessor<CODEC> acc;
+    uint32_t samples;
+
+    __device__ __forceinline__ Tracer(const RenderArgs& a, const float4* e) : A(a), ent(e), acc(a.g), samples(0) {}
+
+    __device__ __forceinline__ float sample_at(const Ray& r, double t)
+    {
+        ++samples;
+        return sample_trilinear<CODEC>(acc, r.o[0] + r.d[0] * t, r.o[1] + r.d[1] * t, r.o[2] + r.d[2] * t);
+    }
+
+    __device__ __forceinline__ int cell_index(const int c[3]) const
+    {
+        return c[0] + A.cells[0] * (c[1] + A.cells[1] * c[2]);
+    }
+
+    // woodcock_track (render.hpp:106-124)
+    __device__ __forceinline__ bool woodcock(double sigma_maj, const Ray& r, double t0, double t1, Rng& rng,
+                                             double& t_ev, float& v_ev)
+    {
+        if (!(sigma_maj > 0.0))
+            return false;
+        double inv = 1.0 / sigma_maj;
+        double t = t0;
+        for (;;) {
+            t -= log(1.0 - rng.uniform()) * inv;
+            if (t >= t1)
+                return false;
+            float v = sample_at(r, t);
+            double st = tf_extinction(A.tf, ent, double(v));
+            if (rng.uniform() < st * inv) {
+                t_ev = t;
+                v_ev = v;
+                return true;
+            }
+        }
+    }
+
+    // next_event (render.hpp:137-151): DDA over 32^3 macrocells, empty cells draw nothing
+    __device__ __forceinline__ bool next_event(const Ray& r, Rng& rng, double& t_ev, float& v_ev)
+    {
+        Dda d;
+        if (!d.init(A.cells, A.hi, r, 0.0, kInf()))
+            return false;
+        int c[3];
+        double ta, tb;
+        while (d.next(A.cells, c, ta, tb)) {
+            float m = __ldg(A.maj + cell_index(c));
+            if (m == 0.0f)
+                continue; // empty (maj == 0); a zero float majorant also draws nothing
+            if (woodcock(double(m), r, ta, tb, rng, t_ev, v_ev))
+                return true;
+        }
+        return false;
+    }
+
+    __device__ __forceinline__ void isotropic(Rng& rng, double d[3])
+    {
+        double z = 1.0 - 2.0 * rng.uniform();
+        double phi = 2.0 * kPi * rng.uniform();
+        double r = sqrt(dmax(0.0, 1.0 - z * z));
+        d[0] = r * cos(phi);
+        d[1] = r * sin(phi);
+        d[2] = z;
+    }
+
+    __device__ __forceinline__ void scatter_albedo(float v, double tp[3])
+    {
+        double rgba[4];
+        tf_lookup(A.tf, ent, double(v), rgba);
+        tp[0] *= double(float(rgba[0])); // tf.rgb() returns Vec3f (transfer.hpp:58-62)
+        tp[1] *= double(float(rgba[1]));
+        tp[2] *= double(float(rgba[2]));
+    }
+
+    // trace_path (render.hpp:160-187)
+    __device__ void trace_path(Ray ray, Rng& rng, float out[3])
+    {
+        double tp[3] = {1.0, 1.0, 1.0};
+        int bounces = 0;
+        for (;;) {
+            double t;
+            float v;
+            if (!next_event(ray, rng, t, v)) {
+                out[0] = float(tp[0] * double(A.ambient[0]));
+                out[1] = float(tp[1] * double(A.ambient[1]));
+                out[2] = float(tp[2] * double(A.ambient[2]));
+                return;
+            }
+            if (++bounces > A.max_bounces) {
+                out[0] = out[1] = out[2] = 0.0f;
+                return;
+            }
+            scatter_albedo(v, tp);
+            ray.o[0] = ray.o[0] + ray.d[0] * t;
+            ray.o[1] = ray.o[1] + ray.d[1] * t;
+            ray.o[2] = ray.o[2] + ray.d[2] * t;
+            isotropic(rng, ray.d);
+            if (bounces >= A.rr_start) {
+                double survive = dclamp(dmax(tp[0], dmax(tp[1], tp[2])), 0.05, 0.95);
+                if (rng.uniform() >= survive) {
+                    out[0] = out[1] = out[2] = 0.0f;
+                    return;
+                }
+                tp[0] /= survive;
+                tp[1] /= survive;
+                tp[2] /= survive;
+            }
+        }
+    }
+
+    // Ratio-tracked escape + delta-tracked scattering (oracle/svdb_oracle.c trace_ratio).
+    __device__ void trace_ratio(Ray ray, Rng& rng, float out[3])
+    {
+        double tp[3] = {1.0, 1.0, 1.0};
+        double L[3] = {0.0, 0.0, 0.0};
+        int bounces = 0;
+        for (;;) {
+            double Tr = 1.0;
+            bool have = false;
+            double t_ev = 0.0;
+            float v_ev = 0.0f;
+            Dda d;
+            if (d.init(A.cells, A.hi, ray, 0.0, kInf())) {
+                int c[3];
+                double ta, tb;
+                while (Tr > 0.0 && d.next(A.cells, c, ta, tb)) {
+                    float m = __ldg(A.maj + cell_index(c));
+                    if (m == 0.0f)
+                        continue;
+                    double inv = 1.0 / double(m);
+                    double t = ta;
+                    for (;;) {
+                        t -= log(1.0 - rng.uniform()) * inv;
+                        if (t >= tb)
+                            break;
+                        float v = sample_at(ray, t);
+                        double r = tf_extinction(A.tf, ent, double(v)) * inv;
+                        if (!have && rng.uniform() < r) {
+                            have = true;
+                            t_ev = t;
+                            v_ev = v;
+                        }
+                        Tr *= 1.0 - r;
+                        if (!(Tr > 0.0))
+                            break;
+                    }
+                }
+            }
+            L[0] += tp[0] * Tr * double(A.ambient[0]);
+            L[1] += tp[1] * Tr * double(A.ambient[1]);
+            L[2] += tp[2] * Tr * double(A.ambient[2]);
+            if (!have)
+                break;
+            if (++bounces > A.max_bounces)
+                break;
+            scatter_albedo(v_ev, tp);
+            ray.o[0] = ray.o[0] + ray.d[0] * t_ev;
+            ray.o[1] = ray.o[1] + ray.d[1] * t_ev;
+            ray.o[2] = ray.o[2] + ray.d[2] * t_ev;
+            isotropic(rng, ray.d);
+            if (bounces >= A.rr_start) {
+                double survive = dclamp(dmax(tp[0], dmax(tp[1], tp[2])), 0.05, 0.95);
+                if (rng.uniform() >= survive)
+                    break;
+                tp[0] /= survive;
+                tp[1] /= survive;
+                tp[2] /= survive;
+            }
+        }
+        out[0] = float(L[0]);
+        out[1] = float(L[1]);
+        out[2] = float(L[2]);
+    }
+
+    // Emission-absorption march (oracle/svdb_oracle.c trace_ea). Samples falling in an empty
+    // macrocell (majorant 0 => alpha 0 on its whole closed box) contribute exactly nothing, so
+    // the march jumps over runs of empty cells without changing a single sample position.
+    __device__ void trace_ea(const Ray& ray, Rng& rng, float out[3])
+    {
+        double j = rng.uniform();
+        double C[3] = {0.0, 0.0, 0.0}, T = 1.0;
+        double t0 = 0.0, t1 = kInf();
+        const double dt = A.ea_step;
+        if (clip_ray_box(ray, A.hi, t0, t1) && t0 <= t1) {
+            for (long long k = 0;; ++k) {
+                double t = t0 + (double(k) + j) * dt;
+                if (!(t < t1))
+                    break;
+                double p[3] = {ray.o[0] + ray.d[0] * t, ray.o[1] + ray.d[1] * t, ray.o[2] + ray.d[2] * t};
+                int c[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+                    c[a] = int(dclamp(floor(p[a] / 32.0), 0.0, double(A.cells[a] - 1)));
+                if (__ldg(A.maj + cell_index(c)) == 0.0f) {
+                    // exact skip: find this empty cell's exit along the ray and resume at the
+                    // last sample index before it (the per-sample test handles the rest)
+                    double te = t1;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        if (ray.d[a] > 0.0)
+                            te = dmin(te, (double(c[a] + 1) * 32.0 - ray.o[a]) / ray.d[a]);
+                        else if (ray.d[a] < 0.0)
+                            te = dmin(te, (double(c[a]) * 32.0 - ray.o[a]) / ray.d[a]);
+                    }
+                    double kk = floor((te - t0) / dt - j) - 1.0;
+                    if (kk > double(k))
+                        k = (long long)kk;
+                    continue;
+                }
+                ++samples;
+                float v = sample_trilinear<CODEC>(acc, p[0], p[1], p[2]);
+                double rgba[4];
+                tf_lookup(A.tf, ent, double(v), rgba);
+                double a = 1.0 - exp(-(A.tf.scale * rgba[3]) * dt);
+                C[0] += T * a * rgba[0];
+                C[1] += T * a * rgba[1];
+                C[2] += T * a * rgba[2];
+                T *= 1.0 - a;
+                if (T < A.ea_min_t)
+                    break;
+            }
+        }
+        out[0] = float(C[0] + T * double(A.background[0]));
+        out[1] = float(C[1] + T * double(A.background[1]));
+        out[2] = float(C[2] + T * double(A.background[2]));
+    }
+
+    // trace_iso_hit + trace_iso (render.hpp:193-255)
+    __device__ void trace_iso(const Ray& ray, float out[3])
+    {
+        const double step = 0.25, iso = A.iso;
+        bool hit = false;
+        double hit_t = 0.0;
+        Dda d;
+        if (d.init(A.cells, A.hi, ray, 0.0, kInf())) {
+            int c[3];
+            double ta, tb;
+            while (!hit && d.next(A.cells, c, ta, tb)) {
+                int ci = cell_index(c);
+                if (iso < double(__ldg(A.cmin + ci)) || iso > double(__ldg(A.cmax + ci)))
+                    continue;
+                double t_prev = ta;
+                double f_prev = double(sample_at(ray, t_prev)) - iso;
+                if (f_prev == 0.0) {
+                    hit = true;
+                    hit_t = t_prev;
+                    break;
+                }
+                for (double t = ta + step;; t += step) {
+                    t = dmin(t, tb);
+                    double f = double(sample_at(ray, t)) - iso;
+                    if (f == 0.0 || (f_prev < 0.0) != (f < 0.0)) {
+                        double a = t_prev, b = t;
+                        for (int i = 0; i < 16; ++i) {
+                            double m = 0.5 * (a + b);
+                            double fm = double(sample_at(ray, m)) - iso;
+                            if (fm == 0.0) {
+                                a = b = m;
+                                break;
+                            }
+                            if ((f_prev < 0.0) == (fm < 0.0))
+                                a = m;
+                            else
+                                b = m;
+                        }
+                        hit = true;
+                        hit_t = 0.5 * (a + b);
+                        break;
+                    }
+                    t_prev = t;
+                    f_prev = f;
+                    if (t >= tb)
+                        break;
+                }
+            }
+        }
+        if (!hit) {
+            out[0] = A.background[0];
+            out[1] = A.background[1];
+            out[2] = A.background[2];
+            return;
+        }
+        double p[3] = {ray.o[0] + ray.d[0] * hit_t, ray.o[1] + ray.d[1] * hit_t, ray.o[2] + ray.d[2] * hit_t};
+        const double h = 0.5;
+        samples += 6;
+        double gx = (double(sample_trilinear<CODEC>(acc, p[0] + h, p[1], p[2])) - double(sample_trilinear<CODEC>(acc, p[0] - h, p[1], p[2]))) / (2.0 * h);
+        double gy = (double(sample_trilinear<CODEC>(acc, p[0], p[1] + h, p[2])) - double(sample_trilinear<CODEC>(acc, p[0], p[1] - h, p[2]))) / (2.0 * h);
+        double gz = (double(sample_trilinear<CODEC>(acc, p[0], p[1], p[2] + h)) - double(sample_trilinear<CODEC>(acc, p[0], p[1], p[2] - h))) / (2.0 * h);
+        double len = sqrt(gx * gx + gy * gy + gz * gz);
+        if (len == 0.0) {
+            out[0] = out[1] = out[2] = 0.0f;
+            return;
+        }
+        gx /= len;
+        gy /= len;
+        gz /= len;
+        out[0] = float(fabs(gx));
+        out[1] = float(fabs(gy));
+        out[2] = float(fabs(gz));
+    }
+};
+
+// camera_ray (render.hpp:259-269); the basis and tan_half come exact from the host
+__device__ __forceinline__ Ray camera_ray(const CamArgs& c, double px, double py)
+{
+    double ndc_x = (2.0 * px / double(c.w) - 1.0) * c.tan_half * c.aspect;
+    double ndc_y = (1.0 - 2.0 * py / double(c.h)) * c.tan_half;
+    Ray r;
+    double d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        r.o[a] = c.pos[a];
+        d[a] = c.fwd[a] + c.right[a] * ndc_x + c.up[a] * ndc_y;
+    }
+    double len = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    r.d[0] = d[0] / len;
+    r.d[1] = d[1] / len;
+    r.d[2] = d[2] / len;
+    return r;
+}
+
+template <int CODEC, int MODE>
+__global__ void __launch_bounds__(256) k_render(const __grid_constant__ RenderArgs A)
+{
+    extern __shared__ float4 s_ent[];
+    for (int i = threadIdx.x; i < A.tf.n; i += blockDim.x)
+        s_ent[i] = A.tf_ent[i];
+    __syncthreads();
+
+    const long long k = blockIdx.x; // k-th tile of this rank
+    const long long t = k * A.nranks + A.rank;
+    const int tx = int(t % A.tiles_x) * 16, ty = int(t / A.tiles_x) * 16;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lx = (w & 1) * 8 + (lane & 7), ly = (w >> 1) * 4 + (lane >> 3);
+    const int px = tx + lx, py = ty + ly;
+    uint32_t samples = 0;
+    if (px < A.cam.w && py < A.cam.h) {
+        Tracer<CODEC> tr(A, s_ent);
+        double acc[3] = {0.0, 0.0, 0.0};
+        for (int s = 0; s < A.spp; ++s) {
+            Rng rng = Rng::for_pixel_sample(A.seed_mixed, px, py, s);
+            double jx = rng.uniform();
+            double jy = rng.uniform();
+            Ray ray = camera_ray(A.cam, double(px) + jx, double(py) + jy);
+            float c[3];
+            if constexpr (MODE == SVDBGPU_MODE_PATHTRACE)
+                tr.trace_path(ray, rng, c);
+            else if constexpr (MODE == SVDBGPU_MODE_RATIO)
+                tr.trace_ratio(ray, rng, c);
+            else if constexpr (MODE == SVDBGPU_MODE_EA)
+                tr.trace_ea(ray, rng, c);
+            else
+                tr.trace_iso(ray, c);
+            acc[0] += double(c[0]);
+            acc[1] += double(c[1]);
+            acc[2] += double(c[2]);
+        }
+        acc[0] /= double(A.spp);
+        acc[1] /= double(A.spp);
+        acc[2] /= double(A.spp);
+        size_t o = A.packed ? (size_t(k) * 256 + size_t(ly) * 16 + size_t(lx)) * 3
+                            : (size_t(py) * size_t(A.cam.w) + size_t(px)) * 3;
+        A.out[o] = float(acc[0]);
+        A.out[o + 1] = float(acc[1]);
+        A.out[o + 2] = float(acc[2]);
+        samples = tr.samples;
+    }
+    // per-warp reduction of the sample counter (stats only)
+    unsigned long long s64 = samples;
+#pragma unroll
+    for (int off = 16; off; off >>= 1)
+        s64 += __shfl_xor_sync(0xffffffffu, s64, off);
+    if (lane == 0 && s64)
+        atomicAdd(A.counters, s64);
+}
+
+__global__ void k_unpack(const float* __restrict__ packed, int nranks, long long max_tiles, int w, int h, int tiles_x,
+                         float* __restrict__ rgb)
+{
+    long long n = (long long)w * h;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        int x = int(i % w), y = int(i / w);
+        long long t = (long long)(y >> 4) * tiles_x + (x >> 4);
+        long long r = t % nranks, k = t / nranks;
+        const float* src = packed + ((r * max_tiles + k) * 256 + (y & 15) * 16 + (x & 15)) * 3;
+        rgb[i * 3] = src[0];
+        rgb[i * 3 + 1] = src[1];
+        rgb[i * 3 + 2] = src[2];
+    }
+}
+
+// Host camera basis with the reference's exact expression order (render.hpp:259-265, vec.hpp).
+void host_camera(const svdbgpu_camera* c, CamArgs* o)
+{
+    auto normalize = [](double v[3]) {
+        double len = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+        v[0] /= len;
+        v[1] /= len;
+        v[2] /= len;
+    };
+    auto cross = [](const double a[3], const double b[3], double r[3]) {
+        r[0] = a[1] * b[2] - a[2] * b[1];
+        r[1] = a[2] * b[0] - a[0] * b[2];
+        r[2] = a[0] * b[1] - a[1] * b[0];
+    };
+    double f[3] = {c->look_at[0] - c->position[0], c->look_at[1] - c->position[1], c->look_at[2] - c->position[2]};
+    normalize(f);
+    double r[3], u[3];
+    cross(f, c->up, r);
+    normalize(r);
+    cross(r, f, u);
+    for (int a = 0; a < 3; ++a) {
+        o->pos[a] = c->position[a];
+        o->fwd[a] = f[a];
+        o->right[a] = r[a];
+        o->up[a] = u[a];
+    }
+    volatile double fov = c->fov_y_deg; // keep (fov * pi) / 360 as two roundings
+    o->tan_half = std::tan(fov * 3.14159265358979323846 / 360.0);
+    o->aspect = double(c->width) / double(c->height);
+    o->w = c->width;
+    o->h = c->height;
+}
+
+uint64_t host_mix64(uint64_t x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+} // namespace
+
+int64_t tiles_for_rank(int w, int h, int rank, int nranks)
+{
+    if (w < 1 || h < 1 || nranks < 1 || rank < 0 || rank >= nranks)
+        return 0;
+    int64_t total = int64_t((w + 15) / 16) * ((h + 15) / 16);
+    return total > rank ? (total - rank + nranks - 1) / nranks : 0;
+}
+
+int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const svdbgpu_settings* st, float* d_out,
+           int packed, cudaStream_t s, svdbgpu_stats* stats)
+{
+    if (!cam || !st || !d_out)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "null camera/settings/output");
+    if (cam->width < 1 || cam->height < 1)
+        return fail(Errc::size_mismatch, "image size must be positive");
+    if (st->spp < 1)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "spp must be >= 1");
+    if (st->mode < 0 || st->mode > SVDBGPU_MODE_RATIO)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "unknown render mode");
+    int nranks = st->tile_nranks > 0 ? st->tile_nranks : 1;
+    int rank = st->tile_nranks > 0 ? st->tile_rank : 0;
+    if (rank < 0 || rank >= nranks)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "tile_rank out of range");
+    if (st->mode == SVDBGPU_MODE_EA && !(st->ea_step > 0.0))
+        return fail_code(SVDBGPU_E_INVALID_ARG, "ea_step must be positive");
+    SVDB_CUDA(cudaSetDevice(g->device));
+    RenderArgs A{};
+    if (int rc = g->upload_tf(tf, s, &A.tf))
+        return rc;
+    float range_ms = 0.0f;
+    if (int rc = g->ensure_ranges(s, &range_ms))
+        return rc;
+    SVDB_CUDA(cudaEventRecord(g->ev0, s));
+    if (int rc = majorants(g, A.tf, s))
+        return rc;
+    SVDB_CUDA(cudaEventRecord(g->ev1, s));
+    SVDB_CUDA(cudaMemsetAsync(g->d_counters, 0, 64, s));
+
+    A.g = g->dg;
+    A.tf_ent = g->d_tf;
+    A.maj = g->d_maj;
+    A.cmin = g->d_cmin;
+    A.cmax = g->d_cmax;
+    for (int a = 0; a < 3; ++a) {
+        A.cells[a] = g->cells[a];
+        A.hi[a] = double(g->dg.dims[a] - 1); // world box [0, dims-1] (macrocell.hpp:50-54)
+    }
+    host_camera(cam, &A.cam);
+    A.spp = st->spp;
+    A.max_bounces = st->max_bounces;
+    A.rr_start = st->rr_start_bounce;
+    A.seed_mixed = host_mix64(st->seed);
+    A.iso = st->iso_value;
+    for (int c = 0; c < 3; ++c) {
+        A.ambient[c] = st->ambient[c];
+        A.background[c] = st->background[c];
+    }
+    A.ea_step = st->ea_step;
+    A.ea_min_t = st->ea_min_transmittance;
+    A.rank = rank;
+    A.nranks = nranks;
+    A.tiles_x = (cam->width + 15) / 16;
+    A.out = d_out;
+    A.packed = packed;
+    A.counters = g->d_counters;
+    const int64_t ntiles = tiles_for_rank(cam->width, cam->height, rank, nranks);
+    const size_t smem = sizeof(float4) * size_t(tf->n_entries);
+    cudaEvent_t e2 = nullptr, e3 = nullptr;
+    SVDB_CUDA(cudaEventCreate(&e2));
+    SVDB_CUDA(cudaEventCreate(&e3));
+    SVDB_CUDA(cudaEventRecord(e2, s));
+    if (ntiles > 0) {
+#define LAUNCH_R(C, M) k_render<C, M><<<unsigned(ntiles), 256, smem, s>>>(A)
+#define BY_MODE(C)                                                                             \
+    switch (st->mode) {                                                                        \
+    case SVDBGPU_MODE_PATHTRACE: LAUNCH_R(C, SVDBGPU_MODE_PATHTRACE); break;                    \
+    case SVDBGPU_MODE_ISO: LAUNCH_R(C, SVDBGPU_MODE_ISO); break;                                \
+    case SVDBGPU_MODE_EA: LAUNCH_R(C, SVDBGPU_MODE_EA); break;                                  \
+    default: LAUNCH_R(C, SVDBGPU_MODE_RATIO); break;                                           \
+    }
+        switch (g->codec) {
+        case kCodecF32: BY_MODE(kCodecF32) break;
+        case kCodecUnorm8: BY_MODE(kCodecUnorm8) break;
+        case kCodecAffine8: BY_MODE(kCodecAffine8) break;
+        default: BY_MODE(kCodecAffine4) break;
+        }
+#undef BY_MODE
+#undef LAUNCH_R
+        cudaError_t le = cudaGetLastError();
+        if (le != cudaSuccess) {
+            cudaEventDestroy(e2);
+            cudaEventDestroy(e3);
+            return cuda_fail(le, "k_render launch");
+        }
+    }
+    SVDB_CUDA(cudaEventRecord(e3, s));
+    unsigned long long samples = 0;
+    SVDB_CUDA(cudaMemcpyAsync(&samples, g->d_counters, 8, cudaMemcpyDeviceToHost, s));
+    SVDB_CUDA(cudaStreamSynchronize(s));
+    float rms = 0.0f, mms = 0.0f;
+    cudaEventElapsedTime(&rms, e2, e3);
+    cudaEventElapsedTime(&mms, g->ev0, g->ev1);
+    cudaEventDestroy(e2);
+    cudaEventDestroy(e3);
+    if (stats) {
+        int64_t w = cam->width, h = cam->height;
+        int tiles_x = (cam->width + 15) / 16;
+        uint64_t pix = 0;
+        for (int64_t kk = 0; kk < ntiles; ++kk) {
+            int64_t t = kk * nranks + rank;
+            int64_t x0 = (t % tiles_x) * 16, y0 = (t / tiles_x) * 16;
+            pix += uint64_t(std::min<int64_t>(16, w - x0)) * uint64_t(std::min<int64_t>(16, h - y0));
+        }
+        stats->paths = pix * uint64_t(st->spp);
+        stats->samples = samples;
+        stats->lookups = samples * 8;
+        stats->render_ms = rms;
+        stats->macrocell_ms = double(range_ms) + double(mms);
+        stats->launches = (range_ms > 0.0f ? 1u : 0u) + 1u + (ntiles > 0 ? 1u : 0u);
+    }
+    return 0;
+}
+
+int unpack_tiles(const float* d_packed, int nranks, int64_t max_tiles, int w, int h, float* d_rgb, cudaStream_t s)
+{
+    if (nranks < 1 || w < 1 || h < 1)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "bad unpack geometry");
+    long long n = (long long)w * h;
+    int blocks = int(std::min<long long>((n + 255) / 256, 148 * 32));
+    k_unpack<<<blocks, 256, 0, s>>>(d_packed, nranks, max_tiles, w, h, (w + 15) / 16, d_rgb);
+    SVDB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+} // namespace svdbgpu
