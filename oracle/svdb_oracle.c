@@ -699,9 +699,9 @@ static void trace_iso(ctx_t* cx, const ray_t* ray, float out[3])
     ray_at(ray, hit_t, p);
     /* sample_gradient (sample.hpp:81-95), h = 0.5 */
     const double h = 0.5;
-    double gx = ((double)sample_trilinear(&cx->acc, p[0] + h, p[1], p[2]) - (double)sample_trilinear(&cx->acc, p[0] - h, p[1], p[2])) / (2.0 * h);
-    double gy = ((double)sample_trilinear(&cx->acc, p[0], p[1] + h, p[2]) - (double)sample_trilinear(&cx->acc, p[0], p[1] - h, p[2])) / (2.0 * h);
-    double gz = ((double)sample_trilinear(&cx->acc, p[0], p[1], p[2] + h) - (double)sample_trilinear(&cx->acc, p[0], p[1], p[2] - h)) / (2.0 * h);
+    double gx = (double)(sample_trilinear(&cx->acc, p[0] + h, p[1], p[2]) - sample_trilinear(&cx->acc, p[0] - h, p[1], p[2])) / (2.0 * h);
+    double gy = (double)(sample_trilinear(&cx->acc, p[0], p[1] + h, p[2]) - sample_trilinear(&cx->acc, p[0], p[1] - h, p[2])) / (2.0 * h);
+    double gz = (double)(sample_trilinear(&cx->acc, p[0], p[1], p[2] + h) - sample_trilinear(&cx->acc, p[0], p[1], p[2] - h)) / (2.0 * h);
     double len = sqrt(gx * gx + gy * gy + gz * gz);
     if (len == 0.0) { out[0] = out[1] = out[2] = 0.0f; return; }
     gx /= len; gy /= len; gz /= len;

@@ -155,9 +155,9 @@ __global__ void k_gradient(DevGrid g, const double* __restrict__ xyz, size_t n, 
         Accessor<CODEC> a(g);
         double x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
         const double h = 0.5;
-        out[3 * i] = (double(sample_trilinear<CODEC>(a, x + h, y, z)) - double(sample_trilinear<CODEC>(a, x - h, y, z))) / (2.0 * h);
-        out[3 * i + 1] = (double(sample_trilinear<CODEC>(a, x, y + h, z)) - double(sample_trilinear<CODEC>(a, x, y - h, z))) / (2.0 * h);
-        out[3 * i + 2] = (double(sample_trilinear<CODEC>(a, x, y, z + h)) - double(sample_trilinear<CODEC>(a, x, y, z - h))) / (2.0 * h);
+        out[3 * i] = double(sample_trilinear<CODEC>(a, x + h, y, z) - sample_trilinear<CODEC>(a, x - h, y, z)) / (2.0 * h);
+        out[3 * i + 1] = double(sample_trilinear<CODEC>(a, x, y + h, z) - sample_trilinear<CODEC>(a, x, y - h, z)) / (2.0 * h);
+        out[3 * i + 2] = double(sample_trilinear<CODEC>(a, x, y, z + h) - sample_trilinear<CODEC>(a, x, y, z - h)) / (2.0 * h);
     }
 }
 

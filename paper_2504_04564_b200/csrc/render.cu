@@ -341,9 +341,9 @@ struct Tracer {
         double p[3] = {ray.o[0] + ray.d[0] * hit_t, ray.o[1] + ray.d[1] * hit_t, ray.o[2] + ray.d[2] * hit_t};
         const double h = 0.5;
         samples += 6;
-        double gx = (double(sample_trilinear<CODEC>(acc, p[0] + h, p[1], p[2])) - double(sample_trilinear<CODEC>(acc, p[0] - h, p[1], p[2]))) / (2.0 * h);
-        double gy = (double(sample_trilinear<CODEC>(acc, p[0], p[1] + h, p[2])) - double(sample_trilinear<CODEC>(acc, p[0], p[1] - h, p[2]))) / (2.0 * h);
-        double gz = (double(sample_trilinear<CODEC>(acc, p[0], p[1], p[2] + h)) - double(sample_trilinear<CODEC>(acc, p[0], p[1], p[2] - h))) / (2.0 * h);
+        double gx = double(sample_trilinear<CODEC>(acc, p[0] + h, p[1], p[2]) - sample_trilinear<CODEC>(acc, p[0] - h, p[1], p[2])) / (2.0 * h);
+        double gy = double(sample_trilinear<CODEC>(acc, p[0], p[1] + h, p[2]) - sample_trilinear<CODEC>(acc, p[0], p[1] - h, p[2])) / (2.0 * h);
+        double gz = double(sample_trilinear<CODEC>(acc, p[0], p[1], p[2] + h) - sample_trilinear<CODEC>(acc, p[0], p[1], p[2] - h)) / (2.0 * h);
         double len = sqrt(gx * gx + gy * gy + gz * gz);
         if (len == 0.0) {
             out[0] = out[1] = out[2] = 0.0f;
