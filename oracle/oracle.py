@@ -52,6 +52,14 @@ class _Settings(C.Structure):
                 ("tile_rank", C.c_int), ("tile_nranks", C.c_int), ("threads", C.c_int)]
 
 
+def _take_bytes(ptr, n: int) -> bytes:
+    # ctypes.string_at takes a C int size: copy > 2 GiB buffers through memmove instead
+    buf = bytearray(n)
+    if n:
+        C.memmove((C.c_char * n).from_buffer(buf), ptr, n)
+    return bytes(buf)
+
+
 def _f32p(a):
     return a.ctypes.data_as(C.POINTER(C.c_float))
 
@@ -123,7 +131,7 @@ class Oracle:
                                   codes.ctypes.data, params.ctypes.data)
         if rc:
             raise OracleError(rc, "quantize")
-        data = C.string_at(out, n_out.value)
+        data = _take_bytes(out, n_out.value)
         self.lib.so_free(out)
         return data, codes[:n_leaf], params[:n_leaf]
 
@@ -247,7 +255,7 @@ class Reference:
             raise OracleError(rc, f"{what}: {self.lib.ref_last_error().decode()}")
 
     def _take(self, p, n):
-        data = C.string_at(p, n.value)
+        data = _take_bytes(p, n.value)
         self.lib.ref_free(p)
         return data
 

@@ -52,6 +52,14 @@ class Error(RuntimeError):
 E_CUDA, E_INVALID_ARG, E_NO_DEVICE, E_OOM, E_UNSUPPORTED = 64, 65, 66, 67, 68
 
 
+def _take_bytes(ptr, n: int) -> bytes:
+    # ctypes.string_at takes a C int size: copy > 2 GiB buffers through memmove instead
+    buf = bytearray(n)
+    if n:
+        C.memmove((C.c_char * n).from_buffer(buf), ptr, n)
+    return bytes(buf)
+
+
 def _check(rc: int):
     if rc:
         msg = N.lib().svdbgpu_last_error()
@@ -119,7 +127,7 @@ def compress(volume: np.ndarray, params: CompressionParams = CompressionParams()
     L = N.lib()
     _check(L.svdbgpu_compress(vol.ctypes.data, dims, int(voxel_type), float(params.quality),
                               int(params.metric), threads, C.byref(out), C.byref(n), C.byref(rep)))
-    data = C.string_at(out, n.value)
+    data = _take_bytes(out, n.value)
     L.svdbgpu_free(out)
     return data, CompressionReport(rep.background, rep.num_bricks, rep.bricks_activated,
                                    rep.voxels_activated, rep.frozen_bytes, rep.dense_bytes,

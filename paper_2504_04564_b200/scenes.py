@@ -29,9 +29,21 @@ class Scene:
     settings: RenderSettings
     tf: TransferFunction
     fov_y_deg: float = 45.0
+    # camera = centre + distance * max_extent * normalize(view); (0,0,-1) at 2.2 is the CLI's
+    # auto-framing (tools/svdb.cpp:267-274); the large configs move in so the volume fills the frame
+    distance: float = 2.2
+    view: tuple = (0.0, 0.0, -1.0)
 
     def camera(self) -> Camera:
-        return frame_camera(self.dims, self.width, self.height, self.fov_y_deg)
+        if self.distance == 2.2 and self.view == (0.0, 0.0, -1.0):
+            return frame_camera(self.dims, self.width, self.height, self.fov_y_deg)
+        ext = [float(d - 1) for d in self.dims]
+        c = [e * 0.5 for e in ext]
+        n = sum(v * v for v in self.view) ** 0.5
+        r = self.distance * max(1.0, max(ext))
+        pos = tuple(c[a] + r * self.view[a] / n for a in range(3))
+        return Camera(position=pos, look_at=tuple(c), fov_y_deg=self.fov_y_deg, width=self.width,
+                      height=self.height)
 
 
 def _tf_ml():
@@ -57,21 +69,27 @@ def _tf_sparse(n):
                                        [0.95, 0.9, 0.85, 1.0]], density_scale=48.0 / n)
 
 
+_NEAR = dict(distance=1.3, view=(0.25, 0.2, -1.0))
+
 SCENES = {
     "C1": Scene("C1", "marschner_lobb", (64, 64, 64), VoxelType.u8, 0, Codec.unorm8, 512, 512,
-                RenderSettings(spp=1, seed=1, mode=RenderMode.ea, ea_step=0.5), _tf_ml()),
+                RenderSettings(spp=1, seed=1, mode=RenderMode.ea, ea_step=0.5), _tf_ml(),
+                distance=1.8, view=(0.3, 0.4, -1.0)),
     "C2": Scene("C2", "fbm_smoke", (256, 256, 256), VoxelType.u8, 2, Codec.unorm8, 1024, 1024,
-                RenderSettings(spp=16, max_bounces=1, rr_start_bounce=3, seed=2), _tf_smoke(256)),
+                RenderSettings(spp=16, max_bounces=1, rr_start_bounce=3, seed=2), _tf_smoke(256),
+                distance=1.6, view=(0.2, 0.3, -1.0)),
     "C3": Scene("C3", "turbulence", (1024, 1024, 1024), VoxelType.f32, 3, Codec.affine8, 1920, 1080,
-                RenderSettings(spp=64, max_bounces=64, rr_start_bounce=3, seed=3), _tf_turbulence(1024)),
+                RenderSettings(spp=64, max_bounces=64, rr_start_bounce=3, seed=3), _tf_turbulence(1024),
+                **_NEAR),
     "C3_4bit": Scene("C3_4bit", "turbulence", (1024, 1024, 1024), VoxelType.f32, 3, Codec.affine4,
                      1920, 1080, RenderSettings(spp=64, max_bounces=64, rr_start_bounce=3, seed=3),
-                     _tf_turbulence(1024)),
+                     _tf_turbulence(1024), **_NEAR),
     "C4": Scene("C4", "sparse", (2048, 2048, 2048), VoxelType.f32, 4, Codec.affine8, 3840, 2160,
                 RenderSettings(spp=16, max_bounces=64, rr_start_bounce=3, seed=4, mode=RenderMode.ratio),
-                _tf_sparse(2048)),
+                _tf_sparse(2048), **_NEAR),
     "C5": Scene("C5", "turbulence", (1024, 1024, 1024), VoxelType.f32, 3, Codec.f32, 1920, 1080,
-                RenderSettings(spp=64, max_bounces=64, rr_start_bounce=3, seed=3), _tf_turbulence(1024)),
+                RenderSettings(spp=64, max_bounces=64, rr_start_bounce=3, seed=3), _tf_turbulence(1024),
+                **_NEAR),
 }
 
 _TF_BY_VOLUME = {"fbm_smoke": _tf_smoke, "turbulence": _tf_turbulence, "sparse": _tf_sparse}
