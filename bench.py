@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto (path-regenerating), 1 per-pixel (A/B)")
+    ap.add_argument("--mode", default="", help="override the integrator: pathtrace|ratio|ea|iso")
     return ap.parse_args()
 
 
@@ -59,9 +61,12 @@ def scene_for(args):
     from dataclasses import replace
     from paper_2504_04564_b200 import scenes as S
     sc = S.scaled(args.config, args.scale, image_factor=1) if args.scale > 1 else S.SCENES[args.config]
-    st = sc.settings
+    import paper_2504_04564_b200 as P
+    st = replace(sc.settings, kernel=args.kernel)
     if args.spp:
         st = replace(st, spp=args.spp)
+    if args.mode:
+        st = replace(st, mode=P.RenderMode[args.mode])
     return replace(sc, width=args.width or sc.width, height=args.height or sc.height, settings=st)
 
 

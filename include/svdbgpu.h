@@ -58,6 +58,9 @@ enum {
     SVDBGPU_MODE_RATIO = 3      /* multi-scatter path, ratio-tracked escape transmittance */
 };
 
+/* Kernel variants for A/B measurement; both produce bit-identical images. */
+enum { SVDBGPU_KERNEL_AUTO = 0, SVDBGPU_KERNEL_PER_PIXEL = 1 };
+
 typedef struct svdbgpu_grid svdbgpu_grid;
 
 /* TransferFunction (transfer.hpp:23-35): evenly spaced RGBA entries over [domain_lo, domain_hi]. */
@@ -85,7 +88,8 @@ typedef struct {
     double ea_step;          /* EA: march step in voxels (default 0.5) */
     double ea_min_transmittance; /* EA: early-out threshold (default 1e-4) */
     int32_t tile_rank, tile_nranks; /* image split: 16x16 tiles t with t % nranks == rank */
-    int32_t reserved[4];
+    int32_t kernel;          /* SVDBGPU_KERNEL_*: 0 auto (path-regenerating tracer), 1 per-pixel */
+    int32_t reserved[3];
 } svdbgpu_settings;
 
 typedef struct {

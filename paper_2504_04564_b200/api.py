@@ -208,12 +208,14 @@ class RenderSettings:
     threads: int = 0
     ea_step: float = 0.5
     ea_min_transmittance: float = 1e-4
+    kernel: int = 0  # 0 auto (path-regenerating tracer), 1 per-pixel (A/B); images identical
 
     def _c(self, tile_rank: int = 0, tile_nranks: int = 1) -> N.Settings:
         return N.Settings(self.spp, self.max_bounces, self.rr_start_bounce, self.seed, int(self.mode),
                           self.iso_value, (C.c_float * 3)(*self.ambient_radiance),
                           (C.c_float * 3)(*self.background_color), self.ea_step,
-                          self.ea_min_transmittance, tile_rank, tile_nranks, (C.c_int32 * 4)())
+                          self.ea_min_transmittance, tile_rank, tile_nranks, self.kernel,
+                          (C.c_int32 * 3)())
 
 
 @dataclass

@@ -432,6 +432,236 @@ __global__ void __launch_bounds__(256) k_render(const __grid_constant__ RenderAr
         atomicAdd(A.counters, s64);
 }
 
+// ---------------------------------------------------------------------------------------------
+// k_trace: persistent, path-regenerating delta/ratio tracker (K4 / K6 production kernel).
+//
+// k_render runs "for each sample: trace the whole path" per lane, so a warp waits for its
+// longest path every sample (ncu: 2.2 active lanes per warp). Here every lane is a small state
+// machine and one loop iteration = one tentative collision: phase A (divergent but ALU-only)
+// advances the lane to its next tentative collision point — starting a new sample or a new
+// pixel, re-entering the DDA after a scatter, skipping empty or exhausted cells — and phase B
+// (re-converged) does the trilinear gather + accept test. Each lane still owns whole pixels and
+// walks their samples in index order with the reference's FP64 arithmetic and draw order, so
+// the image is bit-identical to k_render and to the CPU oracles. Pixels are handed out in 8x4
+// blocks per warp from a global counter (lanes refill individually, so no lane idles at a pixel
+// boundary); the grid is sized to the resident CTA count.
+enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4 };
+
+#ifndef SVDB_TRACE_MIN_BLOCKS
+#define SVDB_TRACE_MIN_BLOCKS 2
+#endif
+template <int CODEC, int MODE>
+__global__ void __launch_bounds__(256, SVDB_TRACE_MIN_BLOCKS) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
+{
+    extern __shared__ float4 s_ent[];
+    for (int i = threadIdx.x; i < A.tf.n; i += blockDim.x)
+        s_ent[i] = A.tf_ent[i];
+    __syncthreads();
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr bool RATIO = MODE == SVDBGPU_MODE_RATIO;
+    const int lane = threadIdx.x & 31;
+    unsigned long long* work = A.counters + 1;
+
+    Tracer<CODEC> tr(A, s_ent);
+    int px = 0, py = 0, s = 0;
+    long long out_off = 0;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    Rng rng{0};
+    Ray ray;
+    double tp0 = 1.0, tp1 = 1.0, tp2 = 1.0;
+    int bounces = 0;
+    Dda dda;
+    double t = 0.0, tb = 0.0, inv = 0.0;
+    double L0 = 0.0, L1 = 0.0, L2 = 0.0, Tr = 1.0, t_ev = 0.0; // ratio tracking
+    float v_ev = 0.0f;
+    bool have = false;
+    int state = kNeedPixel;
+    bool done = false;
+    long long unit = 0;
+    int fill = 32;
+
+    // path finished with float result r (render.hpp:306: accum += Vec3d(c))
+    auto finish_path = [&](float r0, float r1, float r2) {
+        acc0 += double(r0);
+        acc1 += double(r1);
+        acc2 += double(r2);
+        ++s;
+        state = kNeedPath;
+    };
+    auto finish_ratio = [&]() { finish_path(float(L0), float(L1), float(L2)); };
+    // scattering vertex (render.hpp:173-185)
+    auto bounce = [&](double te, float ve) {
+        if (++bounces > A.max_bounces) {
+            if constexpr (RATIO)
+                finish_ratio();
+            else
+                finish_path(0.0f, 0.0f, 0.0f);
+            return;
+        }
+        double tpv[3] = {tp0, tp1, tp2};
+        tr.scatter_albedo(ve, tpv);
+        tp0 = tpv[0];
+        tp1 = tpv[1];
+        tp2 = tpv[2];
+        ray.o[0] = ray.o[0] + ray.d[0] * te;
+        ray.o[1] = ray.o[1] + ray.d[1] * te;
+        ray.o[2] = ray.o[2] + ray.d[2] * te;
+        tr.isotropic(rng, ray.d);
+        if (bounces >= A.rr_start) {
+            double survive = dclamp(dmax(tp0, dmax(tp1, tp2)), 0.05, 0.95);
+            if (rng.uniform() >= survive) {
+                if constexpr (RATIO)
+                    finish_ratio();
+                else
+                    finish_path(0.0f, 0.0f, 0.0f);
+                return;
+            }
+            tp0 /= survive;
+            tp1 /= survive;
+            tp2 /= survive;
+        }
+        state = kNeedSegment;
+    };
+    // the flight left the grid (or Tr hit 0): escape / ratio segment end
+    auto end_segment = [&]() {
+        if constexpr (RATIO) {
+            L0 += tp0 * Tr * double(A.ambient[0]);
+            L1 += tp1 * Tr * double(A.ambient[1]);
+            L2 += tp2 * Tr * double(A.ambient[2]);
+            if (!have)
+                finish_ratio();
+            else
+                bounce(t_ev, v_ev);
+        } else {
+            finish_path(float(tp0 * double(A.ambient[0])), float(tp1 * double(A.ambient[1])),
+                        float(tp2 * double(A.ambient[2])));
+        }
+    };
+
+    for (;;) {
+        // ---- hand out pixels (warp-uniform point) ----
+        unsigned need = __ballot_sync(FULL, state == kNeedPixel && !done);
+        while (need) {
+            if (fill >= 32) {
+                unsigned long long u = 0;
+                if (lane == 0)
+                    u = atomicAdd(work, 1ull);
+                unit = (long long)__shfl_sync(FULL, u, 0);
+                fill = 0;
+                if (unit >= n_units) {
+                    if ((need >> lane) & 1u)
+                        done = true;
+                    break;
+                }
+            }
+            const int below = __popc(need & ((1u << lane) - 1u));
+            const int avail = 32 - fill;
+            if (((need >> lane) & 1u) && below < avail) {
+                const int p = fill + below;
+                const long long k = unit >> 3;
+                const int w = int(unit & 7);
+                const int lx = (w & 1) * 8 + (p & 7), ly = (w >> 1) * 4 + (p >> 3);
+                const long long tt = k * A.nranks + A.rank;
+                px = int(tt % A.tiles_x) * 16 + lx;
+                py = int(tt / A.tiles_x) * 16 + ly;
+                if (px < A.cam.w && py < A.cam.h) {
+                    out_off = A.packed ? (k * 256 + ly * 16 + lx) * 3 : ((long long)py * A.cam.w + px) * 3;
+                    s = 0;
+                    acc0 = acc1 = acc2 = 0.0;
+                    state = kNeedPath;
+                }
+            }
+            const int take = min(__popc(need), avail);
+            fill += take;
+            for (int i = 0; i < take; ++i)
+                need &= need - 1u;
+        }
+        if (__ballot_sync(FULL, !done) == 0)
+            break;
+
+        // ---- phase A: advance to the next tentative collision ----
+        bool point = false;
+        while (!done && state != kNeedPixel && !point) {
+            if (state == kNeedPath) {
+                if (s == A.spp) {
+                    A.out[out_off] = float(acc0 / double(A.spp));
+                    A.out[out_off + 1] = float(acc1 / double(A.spp));
+                    A.out[out_off + 2] = float(acc2 / double(A.spp));
+                    state = kNeedPixel;
+                    break;
+                }
+                rng = Rng::for_pixel_sample(A.seed_mixed, px, py, s);
+                double jx = rng.uniform();
+                double jy = rng.uniform();
+                ray = camera_ray(A.cam, double(px) + jx, double(py) + jy);
+                tp0 = tp1 = tp2 = 1.0;
+                bounces = 0;
+                if constexpr (RATIO)
+                    L0 = L1 = L2 = 0.0;
+                state = kNeedSegment;
+            }
+            if (state == kNeedSegment) {
+                if constexpr (RATIO) {
+                    Tr = 1.0;
+                    have = false;
+                }
+                if (!dda.init(A.cells, A.hi, ray, 0.0, kInf())) {
+                    end_segment();
+                    continue;
+                }
+                state = kNeedCell;
+            }
+            if (state == kNeedCell) {
+                int c[3];
+                double ta, tbb;
+                if ((RATIO && !(Tr > 0.0)) || !dda.next(A.cells, c, ta, tbb)) {
+                    end_segment();
+                    continue;
+                }
+                float m = __ldg(A.maj + tr.cell_index(c));
+                if (m == 0.0f)
+                    continue; // empty cell: no draws (render.hpp:145-146)
+                inv = 1.0 / double(m);
+                t = ta;
+                tb = tbb;
+                state = kInCell;
+            }
+            // kInCell: next tentative collision (render.hpp:116-118)
+            t -= log(1.0 - rng.uniform()) * inv;
+            if (t >= tb)
+                state = kNeedCell;
+            else
+                point = true;
+        }
+
+        // ---- phase B: gather + accept (re-converged) ----
+        if (point) {
+            float v = tr.sample_at(ray, t);
+            double st = tf_extinction(A.tf, tr.ent, double(v));
+            if constexpr (RATIO) {
+                double r = st * inv;
+                if (!have && rng.uniform() < r) {
+                    have = true;
+                    t_ev = t;
+                    v_ev = v;
+                }
+                Tr *= 1.0 - r;
+                if (!(Tr > 0.0))
+                    end_segment();
+            } else {
+                if (rng.uniform() < st * inv)
+                    bounce(t, v);
+            }
+        }
+    }
+    unsigned long long s64 = tr.samples;
+#pragma unroll
+    for (int off = 16; off; off >>= 1)
+        s64 += __shfl_xor_sync(FULL, s64, off);
+    if (lane == 0 && s64)
+        atomicAdd(A.counters, s64);
+}
+
 __global__ void k_unpack(const float* __restrict__ packed, int nranks, long long max_tiles, int w, int h, int tiles_x,
                          float* __restrict__ rgb)
 {
@@ -561,14 +791,31 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     SVDB_CUDA(cudaEventCreate(&e2));
     SVDB_CUDA(cudaEventCreate(&e3));
     SVDB_CUDA(cudaEventRecord(e2, s));
+    const bool wave = st->kernel != SVDBGPU_KERNEL_PER_PIXEL &&
+                      (st->mode == SVDBGPU_MODE_PATHTRACE || st->mode == SVDBGPU_MODE_RATIO);
     if (ntiles > 0) {
+        int sms = 148, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const long long n_units = ntiles * 8;
+#define LAUNCH_T(C, M)                                                                         \
+    {                                                                                          \
+        int per_sm = 1;                                                                        \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace<C, M>, 256, smem);      \
+        long long blocks = std::min<long long>((long long)std::max(per_sm, 1) * sms, (n_units + 7) / 8); \
+        k_trace<C, M><<<unsigned(blocks), 256, smem, s>>>(A, n_units);                         \
+    }
 #define LAUNCH_R(C, M) k_render<C, M><<<unsigned(ntiles), 256, smem, s>>>(A)
 #define BY_MODE(C)                                                                             \
     switch (st->mode) {                                                                        \
-    case SVDBGPU_MODE_PATHTRACE: LAUNCH_R(C, SVDBGPU_MODE_PATHTRACE); break;                    \
+    case SVDBGPU_MODE_PATHTRACE:                                                               \
+        if (wave) LAUNCH_T(C, SVDBGPU_MODE_PATHTRACE) else LAUNCH_R(C, SVDBGPU_MODE_PATHTRACE); \
+        break;                                                                                 \
     case SVDBGPU_MODE_ISO: LAUNCH_R(C, SVDBGPU_MODE_ISO); break;                                \
     case SVDBGPU_MODE_EA: LAUNCH_R(C, SVDBGPU_MODE_EA); break;                                  \
-    default: LAUNCH_R(C, SVDBGPU_MODE_RATIO); break;                                           \
+    default:                                                                                   \
+        if (wave) LAUNCH_T(C, SVDBGPU_MODE_RATIO) else LAUNCH_R(C, SVDBGPU_MODE_RATIO);         \
+        break;                                                                                 \
     }
         switch (g->codec) {
         case kCodecF32: BY_MODE(kCodecF32) break;
