@@ -83,10 +83,11 @@ def lib():
     """Load libsvdbgpu.so once. Raises (never falls back) if it has not been built."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise ImportError(f"{LIB_PATH} not built: run `make -C paper_2504_04564_b200/csrc` "
+        path = os.environ.get("SVDBGPU_LIB", LIB_PATH)  # A/B builds (csrc/Makefile `variants`)
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not built: run `make -C paper_2504_04564_b200/csrc` "
                               "(or __graft_entry__.build()); there is no CPU fallback")
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             f = getattr(L, name)
             f.restype = res

@@ -194,13 +194,19 @@ __device__ __forceinline__ float sample_trilinear(Accessor<CODEC>& a, double px,
         v011 = decode<CODEC>(*a.g, a.leaf, vi + 72, a.lo, a.sc);
         v111 = decode<CODEC>(*a.g, a.leaf, vi + 73, a.lo, a.sc);
     } else {
-        v100 = a.read(x0 + 1, y0, z0);
-        v010 = a.read(x0, y0 + 1, z0);
-        v110 = a.read(x0 + 1, y0 + 1, z0);
-        v001 = a.read(x0, y0, z0 + 1);
-        v101 = a.read(x0 + 1, y0, z0 + 1);
-        v011 = a.read(x0, y0 + 1, z0 + 1);
-        v111 = a.read(x0 + 1, y0 + 1, z0 + 1);
+        // taps straddle leaves (~1/3 of samples): one rolled loop keeps a single copy of the
+        // accessor walk in the instruction stream; tap order as sample.hpp:56-63
+        double v[8];
+#pragma unroll 1
+        for (int i = 1; i < 8; ++i)
+            v[i] = a.read(x0 + (i & 1), y0 + ((i >> 1) & 1), z0 + (i >> 2));
+        v100 = v[1];
+        v010 = v[2];
+        v110 = v[3];
+        v001 = v[4];
+        v101 = v[5];
+        v011 = v[6];
+        v111 = v[7];
     }
     double v00 = v000 * (1.0 - wx) + v100 * wx;
     double v10 = v010 * (1.0 - wx) + v110 * wx;
@@ -373,12 +379,13 @@ struct Dda {
     {
         if (done)
             return false;
-        int axis = 0;
-        if (t_next[1] < t_next[axis])
-            axis = 1;
-        if (t_next[2] < t_next[axis])
-            axis = 2;
-        double tn = axis == 0 ? t_next[0] : (axis == 1 ? t_next[1] : t_next[2]);
+        // axis = 0; if (t_next.y < t_next[axis]) axis = 1; if (t_next.z < t_next[axis]) axis = 2
+        // (dda.hpp:90-94), written with selects so t_next stays in registers
+        const bool ax1 = t_next[1] < t_next[0];
+        const double tm = ax1 ? t_next[1] : t_next[0];
+        const bool ax2 = t_next[2] < tm;
+        const int axis = ax2 ? 2 : (ax1 ? 1 : 0);
+        const double tn = ax2 ? t_next[2] : tm;
         double t_exit = dmin(tn, t1);
         t_exit = dmax(t_exit, t_cur);
         cell[0] = c[0];

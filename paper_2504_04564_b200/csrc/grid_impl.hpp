@@ -42,6 +42,7 @@ struct GridImpl {
     float* d_cmin = nullptr;
     float* d_cmax = nullptr;
     float* d_maj = nullptr;
+    double* d_inv_maj = nullptr; // 1.0 / double(majorant), 0 for empty cells
     bool ranges_valid = false;
     float4* d_tf = nullptr;
     int tf_cap = 0;

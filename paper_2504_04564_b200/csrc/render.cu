@@ -31,6 +31,7 @@ struct RenderArgs {
     DevTF tf;
     const float4* tf_ent;
     const float* maj;
+    const double* inv_maj;
     const float* cmin;
     const float* cmax;
     int cells[3];
@@ -116,8 +117,10 @@ struct Tracer {
         double z = 1.0 - 2.0 * rng.uniform();
         double phi = 2.0 * kPi * rng.uniform();
         double r = sqrt(dmax(0.0, 1.0 - z * z));
-        d[0] = r * cos(phi);
-        d[1] = r * sin(phi);
+        double sp, cp;
+        sincos(phi, &sp, &cp); // same values as sin()/cos(), one argument reduction
+        d[0] = r * cp;
+        d[1] = r * sp;
         d[2] = z;
     }
 
@@ -445,10 +448,16 @@ __global__ void __launch_bounds__(256) k_render(const __grid_constant__ RenderAr
 // the image is bit-identical to k_render and to the CPU oracles. Pixels are handed out in 8x4
 // blocks per warp from a global counter (lanes refill individually, so no lane idles at a pixel
 // boundary); the grid is sized to the resident CTA count.
-enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4 };
+enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4, kPoint = 5, kScatter = 6 };
 
 #ifndef SVDB_TRACE_MIN_BLOCKS
 #define SVDB_TRACE_MIN_BLOCKS 2
+#endif
+#ifndef SVDB_SCHED
+#define SVDB_SCHED 1 // 0: advance-to-point then gather; 1: per-iteration phase selection
+#endif
+#ifndef SVDB_W_SAMPLE
+#define SVDB_W_SAMPLE 1
 #endif
 template <int CODEC, int MODE>
 __global__ void __launch_bounds__(256, SVDB_TRACE_MIN_BLOCKS) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
@@ -531,10 +540,94 @@ __global__ void __launch_bounds__(256, SVDB_TRACE_MIN_BLOCKS) k_trace(const __gr
             if (!have)
                 finish_ratio();
             else
-                bounce(t_ev, v_ev);
+                state = kScatter;
         } else {
             finish_path(float(tp0 * double(A.ambient[0])), float(tp1 * double(A.ambient[1])),
                         float(tp2 * double(A.ambient[2])));
+        }
+    };
+    // kNeedPath / kNeedSegment: write a finished pixel, start the next sample (render.hpp:298-302),
+    // or enter the macrocell DDA with a new flight (render.hpp:142)
+    auto do_start = [&]() {
+        if (state == kScatter) { // the only copy of the scattering code in the loop
+            bounce(t_ev, v_ev);
+            if (state == kNeedSegment)
+                goto segment;
+        }
+        if (state == kNeedPath) {
+            if (s == A.spp) {
+                A.out[out_off] = float(acc0 / double(A.spp));
+                A.out[out_off + 1] = float(acc1 / double(A.spp));
+                A.out[out_off + 2] = float(acc2 / double(A.spp));
+                state = kNeedPixel;
+                return;
+            }
+            rng = Rng::for_pixel_sample(A.seed_mixed, px, py, s);
+            double jx = rng.uniform();
+            double jy = rng.uniform();
+            ray = camera_ray(A.cam, double(px) + jx, double(py) + jy);
+            tp0 = tp1 = tp2 = 1.0;
+            bounces = 0;
+            if constexpr (RATIO)
+                L0 = L1 = L2 = 0.0;
+            state = kNeedSegment;
+        }
+    segment:
+        if constexpr (RATIO) {
+            Tr = 1.0;
+            have = false;
+        }
+        if (!dda.init(A.cells, A.hi, ray, 0.0, kInf())) {
+            end_segment();
+            return;
+        }
+        state = kNeedCell;
+    };
+    // kNeedCell -> next macrocell (empty cells draw nothing, render.hpp:145-146);
+    // kInCell -> one tentative step t -= ln(1-u)/sigma_maj (render.hpp:116-118)
+    auto do_advance = [&]() {
+        if (state == kNeedCell) {
+            int c[3];
+            double ta, tbb;
+            if ((RATIO && !(Tr > 0.0)) || !dda.next(A.cells, c, ta, tbb)) {
+                end_segment();
+                return;
+            }
+            // 1.0 / double(majorant) precomputed per cell with the same IEEE division
+            // (render.hpp:113); 0 marks an empty cell
+            inv = __ldg(A.inv_maj + tr.cell_index(c));
+            if (inv == 0.0)
+                return;
+            t = ta;
+            tb = tbb;
+        }
+        t -= log(1.0 - rng.uniform()) * inv;
+        state = t >= tb ? kNeedCell : kPoint;
+    };
+    // kPoint: trilinear gather at the tentative collision + accept test (render.hpp:119-122)
+    auto do_sample = [&]() {
+        float v = tr.sample_at(ray, t);
+        double st = tf_extinction(A.tf, tr.ent, double(v));
+        if constexpr (RATIO) {
+            double r = st * inv;
+            if (!have && rng.uniform() < r) {
+                have = true;
+                t_ev = t;
+                v_ev = v;
+            }
+            Tr *= 1.0 - r;
+            if (!(Tr > 0.0))
+                end_segment();
+            else
+                state = kInCell;
+        } else {
+            if (rng.uniform() < st * inv) {
+                t_ev = t;
+                v_ev = v;
+                state = kScatter;
+            } else {
+                state = kInCell;
+            }
         }
     };
 
@@ -576,83 +669,41 @@ __global__ void __launch_bounds__(256, SVDB_TRACE_MIN_BLOCKS) k_trace(const __gr
             for (int i = 0; i < take; ++i)
                 need &= need - 1u;
         }
-        if (__ballot_sync(FULL, !done) == 0)
+        const unsigned live = __ballot_sync(FULL, !done);
+        if (live == 0)
             break;
-
-        // ---- phase A: advance to the next tentative collision ----
-        bool point = false;
-        while (!done && state != kNeedPixel && !point) {
-            if (state == kNeedPath) {
-                if (s == A.spp) {
-                    A.out[out_off] = float(acc0 / double(A.spp));
-                    A.out[out_off + 1] = float(acc1 / double(A.spp));
-                    A.out[out_off + 2] = float(acc2 / double(A.spp));
-                    state = kNeedPixel;
-                    break;
-                }
-                rng = Rng::for_pixel_sample(A.seed_mixed, px, py, s);
-                double jx = rng.uniform();
-                double jy = rng.uniform();
-                ray = camera_ray(A.cam, double(px) + jx, double(py) + jy);
-                tp0 = tp1 = tp2 = 1.0;
-                bounces = 0;
-                if constexpr (RATIO)
-                    L0 = L1 = L2 = 0.0;
-                state = kNeedSegment;
+        if (done)
+            continue; // finished lanes idle until the whole warp is done
+#if SVDB_SCHED == 1
+        // ---- phase selection: run the one phase most lanes are waiting in (weights favour
+        // the gather so its memory latency is paid by as many lanes as possible at once) ----
+        {
+            const int nS = __popc(__ballot_sync(live, state == kPoint));
+            const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell));
+            const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter));
+            const int phase = (nS * SVDB_W_SAMPLE >= nA && nS * SVDB_W_SAMPLE >= nT) ? 2 : (nA >= nT ? 1 : 0);
+            if (phase == 0) {
+                if (state == kNeedPath || state == kNeedSegment || state == kScatter)
+                    do_start();
+            } else if (phase == 1) {
+                if (state == kNeedCell || state == kInCell)
+                    do_advance();
+            } else if (state == kPoint) {
+                do_sample();
             }
-            if (state == kNeedSegment) {
-                if constexpr (RATIO) {
-                    Tr = 1.0;
-                    have = false;
-                }
-                if (!dda.init(A.cells, A.hi, ray, 0.0, kInf())) {
-                    end_segment();
-                    continue;
-                }
-                state = kNeedCell;
-            }
-            if (state == kNeedCell) {
-                int c[3];
-                double ta, tbb;
-                if ((RATIO && !(Tr > 0.0)) || !dda.next(A.cells, c, ta, tbb)) {
-                    end_segment();
-                    continue;
-                }
-                float m = __ldg(A.maj + tr.cell_index(c));
-                if (m == 0.0f)
-                    continue; // empty cell: no draws (render.hpp:145-146)
-                inv = 1.0 / double(m);
-                t = ta;
-                tb = tbb;
-                state = kInCell;
-            }
-            // kInCell: next tentative collision (render.hpp:116-118)
-            t -= log(1.0 - rng.uniform()) * inv;
-            if (t >= tb)
-                state = kNeedCell;
+        }
+#else
+        // ---- divergent advance (ALU only) to the next tentative collision, then one
+        // re-converged gather + accept for every lane that has a point ----
+        while (state != kNeedPixel && state != kPoint) {
+            if (state == kNeedPath || state == kNeedSegment || state == kScatter)
+                do_start();
             else
-                point = true;
+                do_advance();
         }
-
-        // ---- phase B: gather + accept (re-converged) ----
-        if (point) {
-            float v = tr.sample_at(ray, t);
-            double st = tf_extinction(A.tf, tr.ent, double(v));
-            if constexpr (RATIO) {
-                double r = st * inv;
-                if (!have && rng.uniform() < r) {
-                    have = true;
-                    t_ev = t;
-                    v_ev = v;
-                }
-                Tr *= 1.0 - r;
-                if (!(Tr > 0.0))
-                    end_segment();
-            } else {
-                if (rng.uniform() < st * inv)
-                    bounce(t, v);
-            }
-        }
+        if (state == kPoint)
+            do_sample();
+#endif
     }
     unsigned long long s64 = tr.samples;
 #pragma unroll
@@ -761,6 +812,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     A.g = g->dg;
     A.tf_ent = g->d_tf;
     A.maj = g->d_maj;
+    A.inv_maj = g->d_inv_maj;
     A.cmin = g->d_cmin;
     A.cmax = g->d_cmax;
     for (int a = 0; a < 3; ++a) {
