@@ -14,6 +14,7 @@
 #include "grid_impl.hpp"
 
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 
 namespace svdbgpu {
@@ -450,8 +451,11 @@ __global__ void __launch_bounds__(256) k_render(const __grid_constant__ RenderAr
 // boundary); the grid is sized to the resident CTA count.
 enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4, kPoint = 5, kScatter = 6 };
 
+#ifndef SVDB_TRACE_THREADS
+#define SVDB_TRACE_THREADS 64 // 2 warps per CTA, <= 96 registers: 20 resident warps per SM
+#endif
 #ifndef SVDB_TRACE_MIN_BLOCKS
-#define SVDB_TRACE_MIN_BLOCKS 2
+#define SVDB_TRACE_MIN_BLOCKS 10
 #endif
 #ifndef SVDB_SCHED
 #define SVDB_SCHED 1 // 0: advance-to-point then gather; 1: per-iteration phase selection
@@ -460,7 +464,7 @@ enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kIn
 #define SVDB_W_SAMPLE 1
 #endif
 template <int CODEC, int MODE>
-__global__ void __launch_bounds__(256, SVDB_TRACE_MIN_BLOCKS) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
+__global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
 {
     extern __shared__ float4 s_ent[];
     for (int i = threadIdx.x; i < A.tf.n; i += blockDim.x)
@@ -682,6 +686,13 @@ __global__ void __launch_bounds__(256, SVDB_TRACE_MIN_BLOCKS) k_trace(const __gr
             const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell));
             const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter));
             const int phase = (nS * SVDB_W_SAMPLE >= nA && nS * SVDB_W_SAMPLE >= nT) ? 2 : (nA >= nT ? 1 : 0);
+#ifdef SVDB_PHASE_STATS
+            if (lane == __ffs(live) - 1) { // per phase: invocations and participating lanes
+                const int n = phase == 0 ? nT : (phase == 1 ? nA : nS);
+                atomicAdd(A.counters + 2 + 2 * phase, 1ull);
+                atomicAdd(A.counters + 3 + 2 * phase, (unsigned long long)n);
+            }
+#endif
             if (phase == 0) {
                 if (state == kNeedPath || state == kNeedSegment || state == kScatter)
                     do_start();
@@ -853,9 +864,9 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
 #define LAUNCH_T(C, M)                                                                         \
     {                                                                                          \
         int per_sm = 1;                                                                        \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace<C, M>, 256, smem);      \
-        long long blocks = std::min<long long>((long long)std::max(per_sm, 1) * sms, (n_units + 7) / 8); \
-        k_trace<C, M><<<unsigned(blocks), 256, smem, s>>>(A, n_units);                         \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace<C, M>, SVDB_TRACE_THREADS, smem);      \
+        long long blocks = std::min<long long>((long long)std::max(per_sm, 1) * sms, (n_units * 32 + SVDB_TRACE_THREADS - 1) / SVDB_TRACE_THREADS); \
+        k_trace<C, M><<<unsigned(blocks), SVDB_TRACE_THREADS, smem, s>>>(A, n_units);                         \
     }
 #define LAUNCH_R(C, M) k_render<C, M><<<unsigned(ntiles), 256, smem, s>>>(A)
 #define BY_MODE(C)                                                                             \
@@ -888,6 +899,16 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     unsigned long long samples = 0;
     SVDB_CUDA(cudaMemcpyAsync(&samples, g->d_counters, 8, cudaMemcpyDeviceToHost, s));
     SVDB_CUDA(cudaStreamSynchronize(s));
+#ifdef SVDB_PHASE_STATS
+    {
+        unsigned long long c[8];
+        cudaMemcpy(c, g->d_counters, 64, cudaMemcpyDeviceToHost);
+        const char* names[3] = {"start", "advance", "gather"};
+        for (int p = 0; p < 3; ++p)
+            fprintf(stderr, "[phase-stats] %-8s invocations %llu lanes/invocation %.2f\n", names[p], c[2 + 2 * p],
+                    c[2 + 2 * p] ? double(c[3 + 2 * p]) / double(c[2 + 2 * p]) : 0.0);
+    }
+#endif
     float rms = 0.0f, mms = 0.0f;
     cudaEventElapsedTime(&rms, e2, e3);
     cudaEventElapsedTime(&mms, g->ev0, g->ev1);
