@@ -227,6 +227,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2504_04564_b200 as P
+    from paper_2504_04564_b200 import dist as D
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -251,20 +252,16 @@ def run_ours(args):
     max_tiles = P.tiles_for_rank(cam.width, cam.height, 0, world)
     packed = torch.zeros(max_tiles * 768, dtype=torch.float32, device=dev)
     frame = torch.zeros(cam.height * cam.width * 3, dtype=torch.float32, device=dev) if rank == 0 else None
-    gathered = (torch.zeros(world * max_tiles * 768, dtype=torch.float32, device=dev)
-                if (world > 1 and rank == 0) else None)
 
     def step():
         st = P.render_device(grid, sc.tf, cam, sc.settings, packed.data_ptr() if world > 1 else frame.data_ptr(),
                              stream.cuda_stream, packed=world > 1, tile_rank=rank, tile_nranks=world)
         if world > 1:
             with torch.cuda.stream(stream):
+                allp = D.gather_packed(packed, world, rank)  # the only collective (NCCL)
                 if rank == 0:
-                    dist.gather(packed, gather_list=list(gathered.chunk(world)), dst=0)
-                    P.unpack_tiles_device(gathered.data_ptr(), world, max_tiles, cam.width, cam.height,
+                    P.unpack_tiles_device(allp.data_ptr(), world, max_tiles, cam.width, cam.height,
                                           frame.data_ptr(), stream.cuda_stream)
-                else:
-                    dist.gather(packed, dst=0)
         return st
 
     for _ in range(args.warmup):
