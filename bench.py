@@ -140,14 +140,15 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(config_key):
-    """dram bytes per render launch from the committed ncu --set full summary, if any."""
+def ncu_traffic(config_key, paths_per_launch):
+    """DRAM bytes per render launch: the committed `ncu --set full` capture's
+    dram__bytes_read.sum + dram__bytes_write.sum per path (profiles/ncu_render_summary.json)
+    times this launch's paths. None when no capture exists for the config."""
     p = os.path.join(ROOT, "profiles", "ncu_render_summary.json")
     try:
         with open(p) as f:
-            j = json.load(f)
-        e = j.get(config_key) or j.get("default")
-        return e.get("dram_bytes_per_launch"), e
+            e = json.load(f)[config_key]
+        return e["dram_bytes_per_path"] * paths_per_launch, e
     except Exception:
         return None, None
 
@@ -339,7 +340,8 @@ def run_ours(args):
         launch_s = render_max / 1e3 / args.steps
         per_launch_lookups = lookups / args.steps / world
         achieved = per_launch_lookups * SECTOR_BYTES / launch_s / 1e9
-        traffic, prof = ncu_traffic(args.config if args.scale == 1 else f"{args.config}/s{args.scale}")
+        traffic, prof = (ncu_traffic(args.config, paths / args.steps / world)
+                         if args.scale == 1 and args.kernel == 0 and not args.mode else (None, None))
         line = {
             "metric": "Mpaths/s (1024^3 8-bit compressed VDB path tracing; Mlookups/s alongside)",
             "value": value, "unit": "Mpaths/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -358,7 +360,9 @@ def run_ours(args):
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_render (per-launch CUDA events on the render stream)",
+                         "traffic_source": prof.get("report") if prof else None,
+                         "algorithmic_bytes_per_launch": per_launch_lookups * SECTOR_BYTES,
+                         "kernel": "k_trace / k_render (CUDA events around the launch on its stream)",
                          "model": "32 B (one sector) per lattice lookup, 8 lookups per trilinear sample",
                          "peak_source": peak_src},
             "clocks": clk,
