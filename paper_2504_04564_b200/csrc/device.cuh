@@ -1,9 +1,9 @@
 // device.cuh — sm_100a device layout of the frozen {5,4,3} tree and the per-thread hot path:
-// cached accessor, N-bit leaf decode, trilinear reconstruction, transfer function, splitmix64
-// streams and the macrocell DDA. Semantics follow the reference exactly (file:line per function,
-// paths under /root/reference/proj/include/svdb/). Translation units including this header are
-// compiled with -fmad=false so every FP64 expression rounds like the reference's x86-64 build;
-// the only fused op is the explicit fmaf() of the affine leaf decode (bit-identical to C99 fmaf).
+// cached accessor, N-bit leaf decode, apron-backed trilinear reconstruction, transfer function,
+// splitmix64 streams and the macrocell DDA. Semantics follow the reference exactly (file:line per
+// function, paths under /root/reference/proj/include/svdb/). Translation units including this
+// header are compiled with -fmad=false so every FP64 expression rounds like the reference's x86-64
+// build; the only fused op is the explicit fmaf() of the affine leaf decode (== C99 fmaf).
 #pragma once
 
 #include <cstdint>
@@ -28,20 +28,28 @@ __device__ __forceinline__ int leaf_voxel(int x, int y, int z)
 }
 
 // ---- leaf decode ----
+// code -> value; UNORM8 == (float)code / 255.0f for every code (tests/test_oracle.py)
+template <int CODEC>
+__device__ __forceinline__ float decode_code(uint32_t c, float lo, float sc)
+{
+    if constexpr (CODEC == kCodecUnorm8)
+        return __double2float_rn(double(c) * (1.0 / 255.0));
+    else
+        return fmaf(float(c), sc, lo);
+}
+
+// voxel vi (0..511) of leaf `leaf`'s own block
 template <int CODEC>
 __device__ __forceinline__ float decode(const DevGrid& g, uint32_t leaf, int vi, float lo, float sc)
 {
     const uint8_t* base = g.codes + size_t(leaf) * g.leaf_stride;
     if constexpr (CODEC == kCodecF32) {
         return __ldg(reinterpret_cast<const float*>(base) + vi);
-    } else if constexpr (CODEC == kCodecUnorm8) {
-        // == (float)code / 255.0f for every code (exhaustively checked, tests/test_codec.py)
-        return __double2float_rn(double(__ldg(base + vi)) * (1.0 / 255.0));
-    } else if constexpr (CODEC == kCodecAffine8) {
-        return fmaf(float(__ldg(base + vi)), sc, lo);
-    } else {
+    } else if constexpr (CODEC == kCodecAffine4) {
         uint32_t b = __ldg(base + (vi >> 1));
-        return fmaf(float((b >> ((vi & 1) * 4)) & 15u), sc, lo);
+        return decode_code<CODEC>((b >> ((vi & 1) * 4)) & 15u, lo, sc);
+    } else {
+        return decode_code<CODEC>(__ldg(base + vi), lo, sc);
     }
 }
 
@@ -125,11 +133,16 @@ struct Accessor {
         return (x & ~7) == lx && (y & ~7) == ly && (z & ~7) == lz;
     }
 
+    __device__ __forceinline__ bool in_lower(int x, int y, int z) const
+    {
+        return ((x & ~127) == wx) & ((y & ~127) == wy) & ((z & ~127) == wz);
+    }
+
     __device__ __forceinline__ float read(int x, int y, int z)
     {
         if (in_leaf(x, y, z))
             return decode<CODEC>(*g, leaf, leaf_voxel(x, y, z), lo, sc);
-        if ((x & ~127) == wx && (y & ~127) == wy && (z & ~127) == wz)
+        if (in_lower(x, y, z))
             return read_lower(x, y, z);
         int ox = x & ~4095, oy = y & ~4095, oz = z & ~4095;
         if (!(ox == ux && oy == uy && oz == uz)) {
@@ -142,6 +155,29 @@ struct Accessor {
         if (upper < 0)
             return g->background;
         return read_upper(x, y, z);
+    }
+
+    // Make the leaf holding (x,y,z) the cached leaf: no memory traffic on a leaf-cache hit, one
+    // lower-slot load when the lower node is cached, a full walk otherwise. false when (x,y,z)
+    // is not inside a leaf (tile / background / no node).
+    __device__ __forceinline__ bool locate(int x, int y, int z)
+    {
+        if (in_leaf(x, y, z))
+            return true;
+        if (in_lower(x, y, z)) {
+            uint4 e = __ldg(g->lower + size_t(lower) * 4096 + lower_slot(x, y, z));
+            if (e.x != kSlotChild)
+                return false;
+            lx = x & ~7;
+            ly = y & ~7;
+            lz = z & ~7;
+            leaf = e.y;
+            lo = __uint_as_float(e.z);
+            sc = __uint_as_float(e.w);
+            return true;
+        }
+        (void)read(x, y, z);
+        return in_leaf(x, y, z);
     }
 };
 
@@ -176,45 +212,71 @@ __device__ __forceinline__ int lattice_coord(double v)
     return int(f);
 }
 
-template <int CODEC>
-__device__ __forceinline__ float sample_trilinear(Accessor<CODEC>& a, double px, double py, double pz)
+// sample.hpp:65-71: x-lerps, then y, then z, in FP64, rounded to float
+__device__ __forceinline__ float trilerp(const double v[8], double wx, double wy, double wz)
 {
-    int x0 = lattice_coord(px), y0 = lattice_coord(py), z0 = lattice_coord(pz);
-    double wx = px - floor(px), wy = py - floor(py), wz = pz - floor(pz);
-    double v000, v100, v010, v110, v001, v101, v011, v111;
-    v000 = a.read(x0, y0, z0);
-    if (((x0 & 7) != 7) & ((y0 & 7) != 7) & ((z0 & 7) != 7) & a.in_leaf(x0, y0, z0)) {
-        // all eight taps inside the cached leaf: decode directly, no node walk
-        int vi = leaf_voxel(x0, y0, z0);
-        v100 = decode<CODEC>(*a.g, a.leaf, vi + 1, a.lo, a.sc);
-        v010 = decode<CODEC>(*a.g, a.leaf, vi + 8, a.lo, a.sc);
-        v110 = decode<CODEC>(*a.g, a.leaf, vi + 9, a.lo, a.sc);
-        v001 = decode<CODEC>(*a.g, a.leaf, vi + 64, a.lo, a.sc);
-        v101 = decode<CODEC>(*a.g, a.leaf, vi + 65, a.lo, a.sc);
-        v011 = decode<CODEC>(*a.g, a.leaf, vi + 72, a.lo, a.sc);
-        v111 = decode<CODEC>(*a.g, a.leaf, vi + 73, a.lo, a.sc);
-    } else {
-        // taps straddle leaves (~1/3 of samples): one rolled loop keeps a single copy of the
-        // accessor walk in the instruction stream; tap order as sample.hpp:56-63
-        double v[8];
-#pragma unroll 1
-        for (int i = 1; i < 8; ++i)
-            v[i] = a.read(x0 + (i & 1), y0 + ((i >> 1) & 1), z0 + (i >> 2));
-        v100 = v[1];
-        v010 = v[2];
-        v110 = v[3];
-        v001 = v[4];
-        v101 = v[5];
-        v011 = v[6];
-        v111 = v[7];
-    }
-    double v00 = v000 * (1.0 - wx) + v100 * wx;
-    double v10 = v010 * (1.0 - wx) + v110 * wx;
-    double v01 = v001 * (1.0 - wx) + v101 * wx;
-    double v11 = v011 * (1.0 - wx) + v111 * wx;
+    double v00 = v[0] * (1.0 - wx) + v[1] * wx;
+    double v10 = v[2] * (1.0 - wx) + v[3] * wx;
+    double v01 = v[4] * (1.0 - wx) + v[5] * wx;
+    double v11 = v[6] * (1.0 - wx) + v[7] * wx;
     double v0 = v00 * (1.0 - wy) + v10 * wy;
     double v1 = v01 * (1.0 - wy) + v11 * wy;
     return float(v0 * (1.0 - wz) + v1 * wz);
+}
+
+// Apron offset of extended-brick voxel (x,y,z) in [0,8]^3 with at least one coordinate == 8
+// (region r = bits of the axes at 8; see k_build_apron in grid.cu)
+__device__ __forceinline__ int apron_offset(int r, int x, int y, int z)
+{
+    switch (r) {
+    case 1: return y + 8 * z;
+    case 2: return 64 + x + 8 * z;
+    case 4: return 128 + x + 8 * y;
+    case 3: return 192 + z;
+    case 5: return 200 + y;
+    case 6: return 208 + x;
+    default: return 216;
+    }
+}
+
+// One tap of the 9^3 stencil brick of the cached leaf: own block or apron, decoded with the
+// owning block's parameters. All eight taps of a sample are independent loads.
+template <int CODEC>
+__device__ __forceinline__ double brick_tap(const Accessor<CODEC>& a, int x, int y, int z)
+{
+    const uint8_t* base = a.g->codes + size_t(a.leaf) * a.g->leaf_stride;
+    const int r = (x >> 3) | ((y >> 3) << 1) | ((z >> 3) << 2);
+    if (r == 0)
+        return double(decode<CODEC>(*a.g, a.leaf, x + 8 * (y + 8 * z), a.lo, a.sc));
+    const int e = apron_offset(r, x & 7, y & 7, z & 7);
+    if constexpr (CODEC == kCodecF32) {
+        return double(__ldg(reinterpret_cast<const float*>(base + a.g->main_bytes) + e));
+    } else {
+        const float2 p = __ldg(a.g->lparams + size_t(a.leaf) * 8 + r);
+        return double(decode_code<CODEC>(__ldg(base + a.g->main_bytes + e), p.x, p.y));
+    }
+}
+
+template <int CODEC>
+__device__ __forceinline__ float sample_trilinear(Accessor<CODEC>& a, double px, double py, double pz)
+{
+    const int x0 = lattice_coord(px), y0 = lattice_coord(py), z0 = lattice_coord(pz);
+    const double wx = px - floor(px), wy = py - floor(py), wz = pz - floor(pz);
+    double v[8];
+    if (a.locate(x0, y0, z0)) {
+        // base voxel in a leaf: all 8 taps come from that leaf's block + apron
+        const int x = x0 & 7, y = y0 & 7, z = z0 & 7;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            v[i] = brick_tap<CODEC>(a, x + (i & 1), y + ((i >> 1) & 1), z + (i >> 2));
+    } else {
+        // base voxel in a tile / background / outside: per-tap accessor reads (rare in data
+        // regions); tap order as sample.hpp:56-63
+#pragma unroll 1
+        for (int i = 0; i < 8; ++i)
+            v[i] = a.read(x0 + (i & 1), y0 + ((i >> 1) & 1), z0 + (i >> 2));
+    }
+    return trilerp(v, wx, wy, wz);
 }
 
 template <int CODEC>

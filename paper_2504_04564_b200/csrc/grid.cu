@@ -31,20 +31,21 @@ inline bool bit(const uint8_t* words, int i) { return (rd_u64(words + 8 * (i >> 
 // ---- K0: leaf codec, one warp per leaf, 128-bit coalesced loads of the staged records ----
 template <int CODEC>
 __global__ void __launch_bounds__(256) k_leaf_encode(const uint8_t* __restrict__ staging, uint64_t n_leaf,
-                                                     uint8_t* __restrict__ codes, float2* __restrict__ params,
-                                                     int* __restrict__ bad)
+                                                     uint8_t* __restrict__ codes_base, uint32_t stride,
+                                                     float2* __restrict__ params, int* __restrict__ bad)
 {
     const int lane = threadIdx.x & 31;
     const uint64_t leaf = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (leaf >= n_leaf)
         return;
+    uint8_t* codes = codes_base + leaf * stride; // this leaf's 8^3 block (apron follows it)
     const float4* vals = reinterpret_cast<const float4*>(staging + leaf * kLeafRec + 80);
     float4 v[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
         v[j] = __ldg(vals + j * 32 + lane); // floats [4(32j+lane), +4): 512 B per warp step
     if constexpr (CODEC == kCodecF32) {
-        float4* dst = reinterpret_cast<float4*>(codes + leaf * 2048);
+        float4* dst = reinterpret_cast<float4*>(codes);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             dst[j * 32 + lane] = v[j];
@@ -52,7 +53,7 @@ __global__ void __launch_bounds__(256) k_leaf_encode(const uint8_t* __restrict__
             params[leaf] = make_float2(0.0f, 0.0f);
         return;
     } else if constexpr (CODEC == kCodecUnorm8) {
-        uint32_t* dst = reinterpret_cast<uint32_t*>(codes + leaf * 512);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(codes);
         bool ok = true;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -100,10 +101,10 @@ __global__ void __launch_bounds__(256) k_leaf_encode(const uint8_t* __restrict__
         for (int j = 0; j < 4; ++j) {
             uint32_t c0 = q(v[j].x), c1 = q(v[j].y), c2 = q(v[j].z), c3 = q(v[j].w);
             if constexpr (CODEC == kCodecAffine8) {
-                reinterpret_cast<uint32_t*>(codes + leaf * 512)[j * 32 + lane] =
+                reinterpret_cast<uint32_t*>(codes)[j * 32 + lane] =
                     c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
             } else {
-                reinterpret_cast<uint16_t*>(codes + leaf * 256)[j * 32 + lane] =
+                reinterpret_cast<uint16_t*>(codes)[j * 32 + lane] =
                     uint16_t(c0 | (c1 << 4) | (c2 << 8) | (c3 << 12));
             }
         }
@@ -127,6 +128,91 @@ __global__ void k_expand_lower(const uint2* __restrict__ staged, uint64_t n_slot
         }
         lower[i] = o;
     }
+}
+
+// Apron build: leaf L (origin o) also stores the +1 layer of its 9^3 stencil brick — the 217
+// voxels with coordinate 8 on some axis — copied as the neighbour's own codes, plus the
+// neighbour's decode parameters per region (a tile/background neighbour is stored as code 0
+// with (lo = value, scale = 0), so fmaf(0, 0, value) == value). Region r (bits: x, y, z at 8)
+// lies entirely in the neighbour block at o + 8*(r&1, r>>1&1, r>>2&1). Decoding an apron tap
+// therefore reproduces exactly what the reference reads at that voxel (frozen.hpp:82-99).
+__device__ __forceinline__ void apron_entry(int e, int& r, int& x, int& y, int& z)
+{
+    x = y = z = 0;
+    if (e < 64) { r = 1; y = e & 7; z = e >> 3; }
+    else if (e < 128) { r = 2; x = (e - 64) & 7; z = (e - 64) >> 3; }
+    else if (e < 192) { r = 4; x = (e - 128) & 7; y = (e - 128) >> 3; }
+    else if (e < 200) { r = 3; z = e - 192; }
+    else if (e < 208) { r = 5; y = e - 200; }
+    else if (e < 216) { r = 6; x = e - 208; }
+    else { r = 7; }
+}
+
+// Resolve the block at origin (x,y,z): {kind, payload, lo, scale} of the lower slot, or a
+// tile/background value in payload with kind tile.
+__device__ uint4 resolve_block(const DevGrid& g, int x, int y, int z)
+{
+    const uint4 bg = make_uint4(kSlotTile, __float_as_uint(g.background), 0, 0);
+    int u = find_upper(g, x & ~4095, y & ~4095, z & ~4095);
+    if (u < 0)
+        return bg;
+    uint2 ue = __ldg(g.upper + size_t(u) * 32768 + upper_slot(x, y, z));
+    if (ue.x == kSlotTile)
+        return make_uint4(kSlotTile, ue.y, 0, 0);
+    if (ue.x != kSlotChild)
+        return bg;
+    uint4 le = __ldg(g.lower + size_t(ue.y) * 4096 + lower_slot(x, y, z));
+    if (le.x == kSlotChild || le.x == kSlotTile)
+        return le;
+    return bg;
+}
+
+template <int CODEC>
+__global__ void __launch_bounds__(256) k_build_apron(DevGrid g, const int4* __restrict__ lorg, uint64_t n_leaf,
+                                                     const float2* __restrict__ own, int* __restrict__ bad)
+{
+    __shared__ uint4 s_info[8][8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t leaf = uint64_t(blockIdx.x) * 8 + w;
+    const bool live = leaf < n_leaf;
+    if (live && lane >= 1 && lane < 8) {
+        const int4 o = lorg[leaf];
+        uint4 info = resolve_block(g, o.x + 8 * (lane & 1), o.y + 8 * ((lane >> 1) & 1), o.z + 8 * (lane >> 2));
+        s_info[w][lane] = info;
+        float2 p = info.x == kSlotChild ? make_float2(__uint_as_float(info.z), __uint_as_float(info.w))
+                                        : make_float2(__uint_as_float(info.y), 0.0f);
+        g.lparams[leaf * 8 + lane] = p;
+    }
+    if (live && lane == 0)
+        g.lparams[leaf * 8] = own[leaf];
+    __syncwarp();
+    if (!live)
+        return;
+    uint8_t* dst = const_cast<uint8_t*>(g.codes) + leaf * g.leaf_stride + g.main_bytes;
+    bool ok = true;
+    for (int e = lane; e < 217; e += 32) {
+        int r, x, y, z;
+        apron_entry(e, r, x, y, z);
+        const uint4 info = s_info[w][r];
+        const int vi = x + 8 * (y + 8 * z);
+        const uint8_t* nb = g.codes + size_t(info.y) * g.leaf_stride;
+        const float cval = __uint_as_float(info.y);
+        if constexpr (CODEC == kCodecF32) {
+            reinterpret_cast<float*>(dst)[e] = info.x == kSlotChild ? reinterpret_cast<const float*>(nb)[vi] : cval;
+        } else {
+            uint32_t c = 0;
+            if (info.x == kSlotChild) {
+                c = CODEC == kCodecAffine4 ? (nb[vi >> 1] >> ((vi & 1) * 4)) & 15u : nb[vi];
+            } else if (CODEC == kCodecUnorm8) {
+                int q = __float2int_rn(__fmul_rn(cval, 255.0f));
+                ok &= q >= 0 && q <= 255 && __double2float_rn(double(q) * (1.0 / 255.0)) == cval;
+                c = uint32_t(q & 255);
+            }
+            dst[e] = uint8_t(c);
+        }
+    }
+    if (!ok)
+        atomicExch(bad, 1);
 }
 
 // ---- K1 ----
@@ -254,6 +340,7 @@ GridImpl::~GridImpl()
     cudaFree(d_upper);
     cudaFree(d_lower);
     cudaFree(d_codes);
+    cudaFree(d_lparams);
     cudaFree(d_cmin);
     cudaFree(d_cmax);
     cudaFree(d_maj);
@@ -441,7 +528,7 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
     SVDB_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
     SVDB_CUDA(cudaEventCreate(&g->ev0));
     SVDB_CUDA(cudaEventCreate(&g->ev1));
-    SVDB_CUDA(cudaMalloc(&g->d_counters, 64));
+    SVDB_CUDA(cudaMalloc(&g->d_counters, 128)); // [0] samples [1] work queue [2..15] stats
     cudaStream_t s = g->stream;
 
     SVDB_CUDA(cudaMalloc(&g->d_root, sizeof(int4) * h_root.size()));
@@ -451,61 +538,42 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
         SVDB_CUDA(cudaMemcpyAsync(g->d_upper, h_upper.data(), sizeof(uint2) * h_upper.size(), cudaMemcpyHostToDevice, s));
     SVDB_CUDA(cudaMalloc(&g->d_lower, sizeof(uint4) * (h_lower.size() ? h_lower.size() : 1)));
 
-    // ---- leaves: stage records in chunks, encode with the codec ----
+    // leaf origins from the node path (lower origin + slot offset), for the apron build
+    std::vector<int4> h_lorg(size_t(nf ? nf : 1), make_int4(0, 0, 0, 0));
+    for (uint64_t i = 0; i < nl; ++i) {
+        const uint8_t* r = low + kLowerRec * i;
+        const int ox = rd_i32(r), oy = rd_i32(r + 4), oz = rd_i32(r + 8);
+        for (int s2 = 0; s2 < 4096; ++s2) {
+            const uint2 e = h_lower[i * 4096 + s2];
+            if (e.x == kSlotChild)
+                h_lorg[e.y] = make_int4(ox + 8 * (s2 & 15), oy + 8 * ((s2 >> 4) & 15), oz + 8 * (s2 >> 8), 0);
+        }
+    }
+
+    // ---- leaves: stage records in chunks, encode with the codec, then build the aprons ----
     int resolved = codec;
     if (codec == SVDBGPU_CODEC_AUTO8)
         resolved = vt == 0 ? kCodecUnorm8 : kCodecAffine8;
-    const uint32_t stride = resolved == kCodecF32 ? 2048u : (resolved == kCodecAffine4 ? 256u : 512u);
+    const uint32_t main_bytes = resolved == kCodecF32 ? 2048u : (resolved == kCodecAffine4 ? 256u : 512u);
+    const uint32_t stride = main_bytes + (resolved == kCodecF32 ? 880u : 256u); // + 217-entry apron
     float2* d_params = nullptr;
     uint2* d_lstage = nullptr;
     uint8_t* d_stage = nullptr;
+    int4* d_lorg = nullptr;
     int* d_bad = nullptr;
     const uint64_t chunk = std::min<uint64_t>(nf ? nf : 1, 1ull << 18); // 256 Ki leaves = 558 MB staging
     SVDB_CUDA(cudaMalloc(&d_params, sizeof(float2) * (nf ? nf : 1)));
     SVDB_CUDA(cudaMalloc(&d_bad, sizeof(int)));
     SVDB_CUDA(cudaMalloc(&g->d_codes, size_t(stride) * (nf ? nf : 1)));
-    if (nf)
-        SVDB_CUDA(cudaMalloc(&d_stage, size_t(kLeafRec * chunk)));
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        SVDB_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
-        for (uint64_t first = 0; first < nf; first += chunk) {
-            uint64_t cnt = std::min(chunk, nf - first);
-            SVDB_CUDA(cudaMemcpyAsync(d_stage, leaf + kLeafRec * first, size_t(kLeafRec * cnt), cudaMemcpyHostToDevice, s));
-            unsigned blocks = unsigned((cnt + 7) / 8);
-            uint8_t* dst = g->d_codes + size_t(stride) * first;
-            float2* par = d_params + first;
-#define LAUNCH_ENCODE(C) k_leaf_encode<C><<<blocks, 256, 0, s>>>(d_stage, cnt, dst, par, d_bad)
-            SVDB_CODEC_DISPATCH(resolved, LAUNCH_ENCODE)
-#undef LAUNCH_ENCODE
-            SVDB_CUDA(cudaGetLastError());
-        }
-        int bad = 0;
-        SVDB_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-        SVDB_CUDA(cudaStreamSynchronize(s));
-        if (!bad)
-            break;
-        if (codec == SVDBGPU_CODEC_AUTO8 && resolved == kCodecUnorm8) {
-            resolved = kCodecAffine8; // same stride
-            continue;
-        }
-        cudaFree(d_stage);
-        cudaFree(d_params);
-        cudaFree(d_bad);
-        return fail(Errc::size_mismatch, "UNORM8 codec needs every leaf value to be byte/255 exact");
-    }
-    cudaFree(d_stage);
-    cudaFree(d_bad);
+    SVDB_CUDA(cudaMalloc(&g->d_lparams, sizeof(float2) * 8 * (nf ? nf : 1)));
+    SVDB_CUDA(cudaMalloc(&d_lorg, sizeof(int4) * h_lorg.size()));
+    SVDB_CUDA(cudaMemcpyAsync(d_lorg, h_lorg.data(), sizeof(int4) * h_lorg.size(), cudaMemcpyHostToDevice, s));
     if (nl) {
         SVDB_CUDA(cudaMalloc(&d_lstage, sizeof(uint2) * h_lower.size()));
         SVDB_CUDA(cudaMemcpyAsync(d_lstage, h_lower.data(), sizeof(uint2) * h_lower.size(), cudaMemcpyHostToDevice, s));
-        k_expand_lower<<<grid_blocks(h_lower.size()), 256, 0, s>>>(d_lstage, h_lower.size(), d_params, g->d_lower);
-        SVDB_CUDA(cudaGetLastError());
     }
-    SVDB_CUDA(cudaStreamSynchronize(s));
-    cudaFree(d_lstage);
-    cudaFree(d_params);
-
-    g->codec = resolved;
+    if (nf)
+        SVDB_CUDA(cudaMalloc(&d_stage, size_t(kLeafRec * chunk)));
     g->dg.dims[0] = dims[0];
     g->dg.dims[1] = dims[1];
     g->dg.dims[2] = dims[2];
@@ -515,10 +583,60 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
     g->dg.upper = g->d_upper;
     g->dg.lower = g->d_lower;
     g->dg.codes = g->d_codes;
+    g->dg.lparams = g->d_lparams;
     g->dg.leaf_stride = stride;
-    g->leaf_payload_bytes = uint64_t(stride) * nf + 8 * nf;
+    g->dg.main_bytes = main_bytes;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        SVDB_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+        for (uint64_t first = 0; first < nf; first += chunk) {
+            uint64_t cnt = std::min(chunk, nf - first);
+            SVDB_CUDA(cudaMemcpyAsync(d_stage, leaf + kLeafRec * first, size_t(kLeafRec * cnt), cudaMemcpyHostToDevice, s));
+            unsigned blocks = unsigned((cnt + 7) / 8);
+            uint8_t* dst = g->d_codes + size_t(stride) * first;
+            float2* par = d_params + first;
+#define LAUNCH_ENCODE(C) k_leaf_encode<C><<<blocks, 256, 0, s>>>(d_stage, cnt, dst, stride, par, d_bad)
+            SVDB_CODEC_DISPATCH(resolved, LAUNCH_ENCODE)
+#undef LAUNCH_ENCODE
+            SVDB_CUDA(cudaGetLastError());
+        }
+        if (nl) {
+            k_expand_lower<<<grid_blocks(h_lower.size()), 256, 0, s>>>(d_lstage, h_lower.size(), d_params, g->d_lower);
+            SVDB_CUDA(cudaGetLastError());
+        }
+        if (nf) {
+            unsigned blocks = unsigned((nf + 7) / 8);
+#define LAUNCH_APRON(C) k_build_apron<C><<<blocks, 256, 0, s>>>(g->dg, d_lorg, nf, d_params, d_bad)
+            SVDB_CODEC_DISPATCH(resolved, LAUNCH_APRON)
+#undef LAUNCH_APRON
+            SVDB_CUDA(cudaGetLastError());
+        }
+        int bad = 0;
+        SVDB_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SVDB_CUDA(cudaStreamSynchronize(s));
+        if (!bad)
+            break;
+        if (codec == SVDBGPU_CODEC_AUTO8 && resolved == kCodecUnorm8) {
+            resolved = kCodecAffine8; // same layout
+            continue;
+        }
+        cudaFree(d_stage);
+        cudaFree(d_params);
+        cudaFree(d_bad);
+        cudaFree(d_lorg);
+        cudaFree(d_lstage);
+        return fail(Errc::size_mismatch, "UNORM8 codec needs every leaf value (and tile/background value "
+                                         "adjacent to a leaf) to be byte/255 exact");
+    }
+    cudaFree(d_stage);
+    cudaFree(d_bad);
+    cudaFree(d_lorg);
+    cudaFree(d_lstage);
+    cudaFree(d_params);
+
+    g->codec = resolved;
+    g->leaf_payload_bytes = uint64_t(stride) * nf + 64 * nf;
     g->device_bytes = sizeof(int4) * h_root.size() + sizeof(uint2) * h_upper.size() + sizeof(uint4) * h_lower.size() +
-                      uint64_t(stride) * nf;
+                      uint64_t(stride) * nf + 64 * nf;
     *out = g.release();
     return 0;
 }
@@ -528,9 +646,9 @@ int grid_leaf_codes(const GridImpl* g, uint64_t first, uint64_t count, uint8_t* 
     if (first + count > g->n_leaf)
         return fail_code(SVDBGPU_E_INVALID_ARG, "leaf range out of bounds");
     SVDB_CUDA(cudaSetDevice(g->device));
-    if (codes && count)
-        SVDB_CUDA(cudaMemcpy(codes, g->d_codes + size_t(g->dg.leaf_stride) * first,
-                             size_t(g->dg.leaf_stride) * count, cudaMemcpyDeviceToHost));
+    if (codes && count) // the leaf's own 8^3 block (the apron behind it is derived data)
+        SVDB_CUDA(cudaMemcpy2D(codes, g->dg.main_bytes, g->d_codes + size_t(g->dg.leaf_stride) * first,
+                               g->dg.leaf_stride, g->dg.main_bytes, count, cudaMemcpyDeviceToHost));
     if (params && count) {
         // params live folded in the lower table; recover them by scanning it on the host
         std::vector<uint4> low(size_t(g->n_lower) * 4096);

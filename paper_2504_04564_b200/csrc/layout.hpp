@@ -22,7 +22,9 @@ struct DevGrid {
     const uint2* upper;
     const uint4* lower;
     const uint8_t* codes;
-    uint32_t leaf_stride; // bytes per leaf: 2048 f32, 512 u8, 256 u4
+    float2* lparams;      // 8 x (lo, scale) per leaf: [0] own, [1..7] apron regions
+    uint32_t leaf_stride; // bytes per leaf: own block (main_bytes) + 217-entry apron
+    uint32_t main_bytes;  // 2048 f32, 512 u8, 256 u4
 };
 
 struct DevTF {

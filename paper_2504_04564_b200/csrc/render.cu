@@ -463,6 +463,9 @@ enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kIn
 #ifndef SVDB_W_SAMPLE
 #define SVDB_W_SAMPLE 1
 #endif
+#ifndef SVDB_COLD_SHARED
+#define SVDB_COLD_SHARED 1
+#endif
 template <int CODEC, int MODE>
 __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
 {
@@ -476,18 +479,47 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
     unsigned long long* work = A.counters + 1;
 
     Tracer<CODEC> tr(A, s_ent);
+    Rng rng{0};
+    Ray ray;
+    Dda dda;
+    double t = 0.0, tb = 0.0, inv = 0.0;
+#if SVDB_COLD_SHARED
+    // Per-lane state touched only at sample start/end, scatter and pixel output lives in shared
+    // memory (SoA, conflict-free), keeping the step/gather loop's register footprint small.
+    __shared__ double s_cold_d[13][SVDB_TRACE_THREADS];
+    __shared__ int s_cold_i[6][SVDB_TRACE_THREADS];
+    const int tid = threadIdx.x;
+    volatile double &acc0 = s_cold_d[0][tid], &acc1 = s_cold_d[1][tid], &acc2 = s_cold_d[2][tid];
+    volatile double &tp0 = s_cold_d[3][tid], &tp1 = s_cold_d[4][tid], &tp2 = s_cold_d[5][tid];
+    volatile double &L0 = s_cold_d[6][tid], &L1 = s_cold_d[7][tid], &L2 = s_cold_d[8][tid];
+    volatile double &Tr = s_cold_d[9][tid], &t_ev = s_cold_d[10][tid];
+    volatile int &px = s_cold_i[0][tid], &py = s_cold_i[1][tid], &s = s_cold_i[2][tid];
+    volatile int &bounces = s_cold_i[3][tid], &out_off = s_cold_i[4][tid];
+    volatile float& v_ev = reinterpret_cast<volatile float&>(s_cold_i[5][tid]);
+    volatile double& have_d = s_cold_d[11][tid]; // ratio: event pending (0/1)
+    struct HaveRef {
+        volatile double& d;
+        __device__ operator bool() const { return d != 0.0; }
+        __device__ HaveRef& operator=(bool b) { d = b ? 1.0 : 0.0; return *this; }
+    } have{have_d};
+    acc0 = acc1 = acc2 = 0.0;
+    tp0 = tp1 = tp2 = 1.0;
+    L0 = L1 = L2 = 0.0;
+    Tr = 1.0;
+    t_ev = 0.0;
+    have = false;
+    px = py = s = bounces = out_off = 0;
+    v_ev = 0.0f;
+#else
     int px = 0, py = 0, s = 0;
     long long out_off = 0;
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-    Rng rng{0};
-    Ray ray;
     double tp0 = 1.0, tp1 = 1.0, tp2 = 1.0;
     int bounces = 0;
-    Dda dda;
-    double t = 0.0, tb = 0.0, inv = 0.0;
     double L0 = 0.0, L1 = 0.0, L2 = 0.0, Tr = 1.0, t_ev = 0.0; // ratio tracking
     float v_ev = 0.0f;
     bool have = false;
+#endif
     int state = kNeedPixel;
     bool done = false;
     long long unit = 0;
@@ -599,7 +631,11 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             }
             // 1.0 / double(majorant) precomputed per cell with the same IEEE division
             // (render.hpp:113); 0 marks an empty cell
+#ifdef SVDB_SOL_NO_MAJ_LOAD // speed-of-light experiment only (wrong images): no majorant load
+            inv = 1.0 / 0.02;
+#else
             inv = __ldg(A.inv_maj + tr.cell_index(c));
+#endif
             if (inv == 0.0)
                 return;
             t = ta;
@@ -608,9 +644,8 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         t -= log(1.0 - rng.uniform()) * inv;
         state = t >= tb ? kNeedCell : kPoint;
     };
-    // kPoint: trilinear gather at the tentative collision + accept test (render.hpp:119-122)
-    auto do_sample = [&]() {
-        float v = tr.sample_at(ray, t);
+    // accept test on the gathered value (render.hpp:119-122) / ratio update
+    auto accept = [&](float v) {
         double st = tf_extinction(A.tf, tr.ent, double(v));
         if constexpr (RATIO) {
             double r = st * inv;
@@ -633,6 +668,16 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
                 state = kInCell;
             }
         }
+    };
+    // kPoint: trilinear gather at the tentative collision + accept test (render.hpp:119-122)
+    auto do_sample = [&]() {
+#ifdef SVDB_SOL_NO_GATHER // speed-of-light experiment only (wrong images): no voxel memory
+        float v = float(t * 1e-3 - floor(t * 1e-3));
+        ++tr.samples;
+#else
+        float v = tr.sample_at(ray, t);
+#endif
+        accept(v);
     };
 
     for (;;) {
@@ -693,6 +738,10 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
                 atomicAdd(A.counters + 3 + 2 * phase, (unsigned long long)n);
             }
 #endif
+#ifdef SVDB_PHASE_STATS
+            __syncwarp(live);
+            const long long c0 = clock64();
+#endif
             if (phase == 0) {
                 if (state == kNeedPath || state == kNeedSegment || state == kScatter)
                     do_start();
@@ -702,6 +751,11 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             } else if (state == kPoint) {
                 do_sample();
             }
+#ifdef SVDB_PHASE_STATS
+            __syncwarp(live);
+            if (lane == __ffs(live) - 1)
+                atomicAdd(A.counters + 8 + phase, (unsigned long long)(clock64() - c0));
+#endif
         }
 #else
         // ---- divergent advance (ALU only) to the next tentative collision, then one
@@ -818,7 +872,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     if (int rc = majorants(g, A.tf, s))
         return rc;
     SVDB_CUDA(cudaEventRecord(g->ev1, s));
-    SVDB_CUDA(cudaMemsetAsync(g->d_counters, 0, 64, s));
+    SVDB_CUDA(cudaMemsetAsync(g->d_counters, 0, 128, s));
 
     A.g = g->dg;
     A.tf_ent = g->d_tf;
@@ -901,12 +955,13 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     SVDB_CUDA(cudaStreamSynchronize(s));
 #ifdef SVDB_PHASE_STATS
     {
-        unsigned long long c[8];
-        cudaMemcpy(c, g->d_counters, 64, cudaMemcpyDeviceToHost);
+        unsigned long long c[16];
+        cudaMemcpy(c, g->d_counters, 128, cudaMemcpyDeviceToHost);
         const char* names[3] = {"start", "advance", "gather"};
         for (int p = 0; p < 3; ++p)
-            fprintf(stderr, "[phase-stats] %-8s invocations %llu lanes/invocation %.2f\n", names[p], c[2 + 2 * p],
-                    c[2 + 2 * p] ? double(c[3 + 2 * p]) / double(c[2 + 2 * p]) : 0.0);
+            fprintf(stderr, "[phase-stats] %-8s invocations %llu lanes/invocation %.2f cycles/invocation %.1f\n",
+                    names[p], c[2 + 2 * p], c[2 + 2 * p] ? double(c[3 + 2 * p]) / double(c[2 + 2 * p]) : 0.0,
+                    c[2 + 2 * p] ? double(c[8 + p]) / double(c[2 + 2 * p]) : 0.0);
     }
 #endif
     float rms = 0.0f, mms = 0.0f;

@@ -51,7 +51,8 @@ def test_u8_sources_unorm8_bit_exact_vs_reference(gpu, ref, name, factor):
     d = sc.dims
     c = all_coords((-2, -2, -2), (d[0] + 2, d[1] + 2, d[2] + 2))
     assert np.array_equal(bits(g.read_voxels(c)), bits(ref.open(svdb).read_voxels(c)))
-    assert g.leaf_payload_bytes == g.counts["leaf"] * (512 + 8)
+    # 512 codes + 217-entry apron (padded to 256) + 8 x (lo, scale) per leaf
+    assert g.leaf_payload_bytes == g.counts["leaf"] * (512 + 256 + 64)
 
 
 @pytest.mark.parametrize("codec", [P.Codec.affine8, P.Codec.affine4])
@@ -153,3 +154,34 @@ def test_svdb_errors_map_to_errc(gpu, ref):
     with pytest.raises(P.Error) as e:
         P.DeviceGrid(bytes(bad))
     assert e.value.code == P.Errc.corrupt_index
+
+
+@pytest.mark.parametrize("codec", [P.Codec.f32, P.Codec.unorm8, P.Codec.affine8, P.Codec.affine4])
+def test_apron_stencils_bit_exact_at_leaf_faces(gpu, orc, ref, codec):
+    """Positions whose 2x2x2 stencil straddles leaf faces/edges/corners, lower-node boundaries,
+    tiles and the volume border: the apron-backed gather must equal the reference sampler on the
+    (dequantised) grid bit for bit."""
+    sc = S.scaled("C2", 2) if codec == P.Codec.unorm8 else S.scaled("C3", 8)
+    _, svdb, _ = scene_svdb(sc)
+    g = P.DeviceGrid(svdb, codec)
+    deq = svdb if codec in (P.Codec.f32, P.Codec.unorm8) else orc.quantize(svdb, int(codec))[0]
+    rg = ref.open(deq)
+    if codec != P.Codec.unorm8:
+        # leaves next to lower-slot tiles, upper-slot tiles and background (apron regions that
+        # come from constants rather than neighbour leaves)
+        ops = mixed_tile_ops(7, 400) + [(2, (128, 0, 0), 2.5), (0, (127, 5, 5), 9.0), (0, (135, 7, 7), 4.0)]
+        tsv = ref.build_ops((200, 72, 72), 0.25, ops)
+        tdeq = tsv if codec == P.Codec.f32 else orc.quantize(tsv, int(codec))[0]
+        gt, rt = P.DeviceGrid(tsv, codec), ref.open(tdeq)
+        pt = np.random.default_rng(5).uniform(-2, 1, size=(80000, 3)) + \
+            np.random.default_rng(6).integers(0, 9, size=(80000, 3)) * 8 + 7
+        pt[:, 0] *= 2.7
+        assert np.array_equal(bits(gt.sample(pt, 1)), bits(rt.sample(pt, 1)))
+    rr = np.random.default_rng(11)
+    n = 60000
+    d = np.array(sc.dims)
+    base = rr.integers(-1, d + 1, size=(n, 3))
+    base[: n // 2] = (base[: n // 2] // 8) * 8 + 7          # x/y/z all at a leaf's last voxel
+    base[n // 2: 3 * n // 4, 0] = (base[n // 2: 3 * n // 4, 0] // 128) * 128 + 127  # lower-node faces
+    p = base + rr.uniform(0, 1, size=(n, 3))
+    assert np.array_equal(bits(g.sample(p, 1)), bits(rg.sample(p, 1)))
