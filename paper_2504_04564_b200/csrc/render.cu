@@ -451,6 +451,87 @@ __global__ void __launch_bounds__(256) k_render(const __grid_constant__ RenderAr
 // boundary); the grid is sized to the resident CTA count.
 enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4, kPoint = 5, kScatter = 6 };
 
+// The macrocell DDA of device.cuh (dda.hpp:52-109), same arithmetic, with its 23 words of
+// per-lane state in shared memory (SoA, conflict-free) instead of registers: it is touched once
+// per cell visit, and the registers it frees buy resident warps for latency hiding.
+template <int T>
+struct SharedDda {
+    volatile int* si;    // [7][T]: c0..2, step0..2, done
+    volatile double* sd; // [8][T]: t_next0..2, t_delta0..2, t_cur, t1
+    int tid;
+    __device__ __forceinline__ volatile int& ci(int k) { return si[k * T + tid]; }
+    __device__ __forceinline__ volatile double& cd(int k) { return sd[k * T + tid]; }
+    __device__ __forceinline__ int cx() { return ci(0); }
+    __device__ __forceinline__ int cy() { return ci(1); }
+    __device__ __forceinline__ int cz() { return ci(2); }
+    __device__ __forceinline__ bool done() { return ci(6) != 0; }
+
+    __device__ __forceinline__ bool init(const int cells[3], const double hi[3], const Ray& r, double t0_, double t1_)
+    {
+        double t0 = t0_, t1 = t1_;
+        if (!clip_ray_box(r, hi, t0, t1))
+            return false;
+        if (!(t0 <= t1))
+            return false;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            double e = r.o[a] + r.d[a] * t0;
+            int c = int(dclamp(floor(e / 32.0), 0.0, double(cells[a] - 1)));
+            double d = r.d[a];
+            int step = 0;
+            double tn = __longlong_as_double(0x7ff0000000000000ll), td = tn;
+            if (d > 0.0) {
+                step = 1;
+                tn = (double(c + 1) * 32.0 - r.o[a]) / d;
+                td = 32.0 / d;
+            } else if (d < 0.0) {
+                step = -1;
+                tn = (double(c) * 32.0 - r.o[a]) / d;
+                td = -32.0 / d;
+            }
+            ci(a) = c;
+            ci(3 + a) = step;
+            cd(a) = tn;
+            cd(3 + a) = td;
+        }
+        cd(6) = t0;
+        cd(7) = t1;
+        ci(6) = 0;
+        return true;
+    }
+
+    __device__ __forceinline__ bool next(const int cells[3], int cell[3], double& ta, double& tb)
+    {
+        if (ci(6))
+            return false;
+        const double n0 = cd(0), n1 = cd(1), n2 = cd(2), t_cur = cd(6), t1 = cd(7);
+        const bool ax1 = n1 < n0;
+        const double tm = ax1 ? n1 : n0;
+        const bool ax2 = n2 < tm;
+        const int axis = ax2 ? 2 : (ax1 ? 1 : 0);
+        const double tn = ax2 ? n2 : tm;
+        double t_exit = dmin(tn, t1);
+        t_exit = dmax(t_exit, t_cur);
+        cell[0] = ci(0);
+        cell[1] = ci(1);
+        cell[2] = ci(2);
+        ta = t_cur;
+        tb = t_exit;
+        if (t_exit >= t1) {
+            ci(6) = 1;
+            return true;
+        }
+        cd(6) = t_exit;
+        const int c = (axis == 0 ? cell[0] : (axis == 1 ? cell[1] : cell[2])) + ci(3 + axis);
+        ci(axis) = c;
+        if (c < 0 || c >= cells[axis])
+            ci(6) = 1;
+        else
+            cd(axis) = (axis == 0 ? n0 : (axis == 1 ? n1 : n2)) + cd(3 + axis);
+        return true;
+    }
+};
+
 #ifndef SVDB_TRACE_THREADS
 #define SVDB_TRACE_THREADS 64 // 2 warps per CTA, <= 96 registers: 20 resident warps per SM
 #endif
@@ -465,6 +546,15 @@ enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kIn
 #endif
 #ifndef SVDB_COLD_SHARED
 #define SVDB_COLD_SHARED 1
+#endif
+#ifndef SVDB_MAJ_AHEAD
+#define SVDB_MAJ_AHEAD 1
+#endif
+#ifndef SVDB_LOCATE_AHEAD
+#define SVDB_LOCATE_AHEAD 0 // measured slower: the extra live registers cost resident warps
+#endif
+#ifndef SVDB_DDA_SHARED
+#define SVDB_DDA_SHARED 1
 #endif
 template <int CODEC, int MODE>
 __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
@@ -481,8 +571,25 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
     Tracer<CODEC> tr(A, s_ent);
     Rng rng{0};
     Ray ray;
+#if SVDB_DDA_SHARED
+    __shared__ int s_dda_i[7][SVDB_TRACE_THREADS];
+    __shared__ double s_dda_d[8][SVDB_TRACE_THREADS];
+    SharedDda<SVDB_TRACE_THREADS> dda{&s_dda_i[0][0], &s_dda_d[0][0], int(threadIdx.x)};
+    auto dda_cur_index = [&]() { return dda.cx() + A.cells[0] * (dda.cy() + A.cells[1] * dda.cz()); };
+    auto dda_done = [&]() { return dda.done(); };
+#else
     Dda dda;
+    auto dda_cur_index = [&]() { return tr.cell_index(dda.c); };
+    auto dda_done = [&]() { return dda.done; };
+#endif
     double t = 0.0, tb = 0.0, inv = 0.0;
+#if SVDB_MAJ_AHEAD
+    double inv_ahead = 0.0;
+#endif
+#if SVDB_LOCATE_AHEAD
+    uint4 pend = make_uint4(0, 0, 0, 0);
+    bool pend_ok = false;
+#endif
 #if SVDB_COLD_SHARED
     // Per-lane state touched only at sample start/end, scatter and pixel output lives in shared
     // memory (SoA, conflict-free), keeping the step/gather loop's register footprint small.
@@ -617,6 +724,9 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             end_segment();
             return;
         }
+#if SVDB_MAJ_AHEAD
+        inv_ahead = __ldg(A.inv_maj + dda_cur_index());
+#endif
         state = kNeedCell;
     };
     // kNeedCell -> next macrocell (empty cells draw nothing, render.hpp:145-146);
@@ -633,6 +743,12 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             // (render.hpp:113); 0 marks an empty cell
 #ifdef SVDB_SOL_NO_MAJ_LOAD // speed-of-light experiment only (wrong images): no majorant load
             inv = 1.0 / 0.02;
+#elif SVDB_MAJ_AHEAD
+            // the majorant of this cell was loaded one visit ahead; issue the next cell's now
+            // (dda.c already holds the following cell) so the load overlaps a whole iteration
+            inv = inv_ahead;
+            if (!dda_done())
+                inv_ahead = __ldg(A.inv_maj + dda_cur_index());
 #else
             inv = __ldg(A.inv_maj + tr.cell_index(c));
 #endif
@@ -643,6 +759,17 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         }
         t -= log(1.0 - rng.uniform()) * inv;
         state = t >= tb ? kNeedCell : kPoint;
+#if SVDB_LOCATE_AHEAD
+        // software pipelining: a new tentative collision issues the lower-slot load naming its
+        // base voxel's leaf now; the gather (a later iteration) starts with the leaf located
+        if (state == kPoint) {
+            const int x0 = lattice_coord(ray.o[0] + ray.d[0] * t), y0 = lattice_coord(ray.o[1] + ray.d[1] * t),
+                      z0 = lattice_coord(ray.o[2] + ray.d[2] * t);
+            pend_ok = !tr.acc.in_leaf(x0, y0, z0) && tr.acc.in_lower(x0, y0, z0);
+            if (pend_ok)
+                pend = __ldg(A.g.lower + size_t(tr.acc.lower) * 4096 + lower_slot(x0, y0, z0));
+        }
+#endif
     };
     // accept test on the gathered value (render.hpp:119-122) / ratio update
     auto accept = [&](float v) {
@@ -675,6 +802,18 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         float v = float(t * 1e-3 - floor(t * 1e-3));
         ++tr.samples;
 #else
+#if SVDB_LOCATE_AHEAD
+        if (pend_ok && pend.x == kSlotChild) {
+            Accessor<CODEC>& a = tr.acc;
+            a.lx = lattice_coord(ray.o[0] + ray.d[0] * t) & ~7;
+            a.ly = lattice_coord(ray.o[1] + ray.d[1] * t) & ~7;
+            a.lz = lattice_coord(ray.o[2] + ray.d[2] * t) & ~7;
+            a.leaf = pend.y;
+            a.lo = __uint_as_float(pend.z);
+            a.sc = __uint_as_float(pend.w);
+        }
+        pend_ok = false;
+#endif
         float v = tr.sample_at(ray, t);
 #endif
         accept(v);
