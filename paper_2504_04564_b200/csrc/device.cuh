@@ -158,26 +158,48 @@ struct Accessor {
     }
 
     // Make the leaf holding (x,y,z) the cached leaf: no memory traffic on a leaf-cache hit, one
-    // lower-slot load when the lower node is cached, a full walk otherwise. false when (x,y,z)
-    // is not inside a leaf (tile / background / no node).
-    __device__ __forceinline__ bool locate(int x, int y, int z)
+    // lower-slot load when the lower node is cached, the root/upper walk otherwise. Returns
+    // false when (x,y,z) is not inside a leaf; `value` then holds the tile / background value
+    // the reference reads there (frozen.hpp:82-99). The only copy of the node walk in the
+    // sampler, so the trace loop stays small.
+    __device__ __forceinline__ bool locate(int x, int y, int z, float& value)
     {
         if (in_leaf(x, y, z))
             return true;
-        if (in_lower(x, y, z)) {
-            uint4 e = __ldg(g->lower + size_t(lower) * 4096 + lower_slot(x, y, z));
-            if (e.x != kSlotChild)
+        if (!in_lower(x, y, z)) {
+            const int ox = x & ~4095, oy = y & ~4095, oz = z & ~4095;
+            if (!(ox == ux && oy == uy && oz == uz)) {
+                ux = ox;
+                uy = oy;
+                uz = oz;
+                upper = find_upper(*g, ox, oy, oz);
+            }
+            value = g->background;
+            if (upper < 0)
                 return false;
-            lx = x & ~7;
-            ly = y & ~7;
-            lz = z & ~7;
-            leaf = e.y;
-            lo = __uint_as_float(e.z);
-            sc = __uint_as_float(e.w);
-            return true;
+            const uint2 ue = __ldg(g->upper + size_t(upper) * 32768 + upper_slot(x, y, z));
+            if (ue.x != kSlotChild) {
+                if (ue.x == kSlotTile)
+                    value = __uint_as_float(ue.y);
+                return false;
+            }
+            wx = x & ~127;
+            wy = y & ~127;
+            wz = z & ~127;
+            lower = ue.y;
         }
-        (void)read(x, y, z);
-        return in_leaf(x, y, z);
+        const uint4 e = __ldg(g->lower + size_t(lower) * 4096 + lower_slot(x, y, z));
+        if (e.x != kSlotChild) {
+            value = e.x == kSlotTile ? __uint_as_float(e.y) : g->background;
+            return false;
+        }
+        lx = x & ~7;
+        ly = y & ~7;
+        lz = z & ~7;
+        leaf = e.y;
+        lo = __uint_as_float(e.z);
+        sc = __uint_as_float(e.w);
+        return true;
     }
 };
 
@@ -262,21 +284,26 @@ __device__ __forceinline__ float sample_trilinear(Accessor<CODEC>& a, double px,
 {
     const int x0 = lattice_coord(px), y0 = lattice_coord(py), z0 = lattice_coord(pz);
     const double wx = px - floor(px), wy = py - floor(py), wz = pz - floor(pz);
-    double v[8];
-    if (a.locate(x0, y0, z0)) {
-        // base voxel in a leaf: all 8 taps come from that leaf's block + apron
-        const int x = x0 & 7, y = y0 & 7, z = z0 & 7;
+    {
+        float c0;
+        if (a.locate(x0, y0, z0, c0)) {
+            // base voxel in a leaf: all 8 taps come from that leaf's block + apron
+            const int x = x0 & 7, y = y0 & 7, z = z0 & 7;
+            double v[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-            v[i] = brick_tap<CODEC>(a, x + (i & 1), y + ((i >> 1) & 1), z + (i >> 2));
-    } else {
+            for (int k = 0; k < 8; ++k)
+                v[k] = brick_tap<CODEC>(a, x + (k & 1), y + ((k >> 1) & 1), z + (k >> 2));
+            return trilerp(v, wx, wy, wz);
+        }
         // base voxel in a tile / background / outside: per-tap accessor reads (rare in data
         // regions); tap order as sample.hpp:56-63
+        double v[8];
+        v[0] = c0;
 #pragma unroll 1
-        for (int i = 0; i < 8; ++i)
+        for (int i = 1; i < 8; ++i)
             v[i] = a.read(x0 + (i & 1), y0 + ((i >> 1) & 1), z0 + (i >> 2));
+        return trilerp(v, wx, wy, wz);
     }
-    return trilerp(v, wx, wy, wz);
 }
 
 template <int CODEC>

@@ -115,8 +115,17 @@ struct Tracer {
 
     __device__ __forceinline__ void isotropic(Rng& rng, double d[3])
     {
-        double z = 1.0 - 2.0 * rng.uniform();
-        double phi = 2.0 * kPi * rng.uniform();
+        double u0 = 0.0, u1 = 0.0;
+#pragma unroll 1
+        for (int k = 0; k < 2; ++k) { // two draws, one copy of the generator in the code
+            const double u = rng.uniform();
+            if (k == 0)
+                u0 = u;
+            else
+                u1 = u;
+        }
+        double z = 1.0 - 2.0 * u0;
+        double phi = 2.0 * kPi * u1;
         double r = sqrt(dmax(0.0, 1.0 - z * z));
         double sp, cp;
         sincos(phi, &sp, &cp); // same values as sin()/cos(), one argument reduction
@@ -365,8 +374,18 @@ struct Tracer {
 // camera_ray (render.hpp:259-269); the basis and tan_half come exact from the host
 __device__ __forceinline__ Ray camera_ray(const CamArgs& c, double px, double py)
 {
-    double ndc_x = (2.0 * px / double(c.w) - 1.0) * c.tan_half * c.aspect;
-    double ndc_y = (1.0 - 2.0 * py / double(c.h)) * c.tan_half;
+    // rolled loops keep one copy of each FP64 division (same operations as render.hpp:266-268)
+    double qx = 0.0, qy = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < 2; ++k) {
+        const double q = 2.0 * (k == 0 ? px : py) / double(k == 0 ? c.w : c.h);
+        if (k == 0)
+            qx = q;
+        else
+            qy = q;
+    }
+    double ndc_x = (qx - 1.0) * c.tan_half * c.aspect;
+    double ndc_y = (1.0 - qy) * c.tan_half;
     Ray r;
     double d[3];
 #pragma unroll
@@ -375,9 +394,16 @@ __device__ __forceinline__ Ray camera_ray(const CamArgs& c, double px, double py
         d[a] = c.fwd[a] + c.right[a] * ndc_x + c.up[a] * ndc_y;
     }
     double len = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-    r.d[0] = d[0] / len;
-    r.d[1] = d[1] / len;
-    r.d[2] = d[2] / len;
+#pragma unroll 1
+    for (int k = 0; k < 3; ++k) {
+        const double q = (k == 0 ? d[0] : (k == 1 ? d[1] : d[2])) / len;
+        if (k == 0)
+            r.d[0] = q;
+        else if (k == 1)
+            r.d[1] = q;
+        else
+            r.d[2] = q;
+    }
     return r;
 }
 
@@ -466,28 +492,48 @@ struct SharedDda {
     __device__ __forceinline__ int cz() { return ci(2); }
     __device__ __forceinline__ bool done() { return ci(6) != 0; }
 
-    __device__ __forceinline__ bool init(const int cells[3], const double hi[3], const Ray& r, double t0_, double t1_)
+    // clip_ray_box + dda_traverse setup (dda.hpp:25-86). Rolled per-axis loops keep one copy of
+    // each FP64 division in the instruction stream (this runs once per flight segment); the
+    // operations and their order per axis are exactly the reference's.
+    __device__ __forceinline__ bool init(const int cells[3], const double hi[3], const Ray& r, double t0, double t1)
     {
-        double t0 = t0_, t1 = t1_;
-        if (!clip_ray_box(r, hi, t0, t1))
-            return false;
+#pragma unroll 1
+        for (int a = 0; a < 3; ++a) {
+            const double o = a == 0 ? r.o[0] : (a == 1 ? r.o[1] : r.o[2]);
+            const double d = a == 0 ? r.d[0] : (a == 1 ? r.d[1] : r.d[2]);
+            const double h = a == 0 ? hi[0] : (a == 1 ? hi[1] : hi[2]);
+            if (d == 0.0) {
+                if (o < 0.0 || o > h)
+                    return false;
+                continue;
+            }
+            const double inv = 1.0 / d;
+            double ta = (0.0 - o) * inv, tb = (h - o) * inv;
+            if (ta > tb) {
+                const double tt = ta;
+                ta = tb;
+                tb = tt;
+            }
+            t0 = dmax(t0, ta);
+            t1 = dmin(t1, tb);
+            if (t0 > t1)
+                return false;
+        }
         if (!(t0 <= t1))
             return false;
-#pragma unroll
+#pragma unroll 1
         for (int a = 0; a < 3; ++a) {
-            double e = r.o[a] + r.d[a] * t0;
-            int c = int(dclamp(floor(e / 32.0), 0.0, double(cells[a] - 1)));
-            double d = r.d[a];
+            const double o = a == 0 ? r.o[0] : (a == 1 ? r.o[1] : r.o[2]);
+            const double d = a == 0 ? r.d[0] : (a == 1 ? r.d[1] : r.d[2]);
+            const int n = a == 0 ? cells[0] : (a == 1 ? cells[1] : cells[2]);
+            const double e = o + d * t0;
+            const int c = int(dclamp(floor(e / 32.0), 0.0, double(n - 1)));
             int step = 0;
             double tn = __longlong_as_double(0x7ff0000000000000ll), td = tn;
-            if (d > 0.0) {
-                step = 1;
-                tn = (double(c + 1) * 32.0 - r.o[a]) / d;
-                td = 32.0 / d;
-            } else if (d < 0.0) {
-                step = -1;
-                tn = (double(c) * 32.0 - r.o[a]) / d;
-                td = -32.0 / d;
+            if (d != 0.0) {
+                step = d > 0.0 ? 1 : -1;
+                tn = (double(d > 0.0 ? c + 1 : c) * 32.0 - o) / d;
+                td = (d > 0.0 ? 32.0 : -32.0) / d;
             }
             ci(a) = c;
             ci(3 + a) = step;
@@ -668,9 +714,15 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
                     finish_path(0.0f, 0.0f, 0.0f);
                 return;
             }
+#if SVDB_COLD_SHARED
+#pragma unroll 1
+            for (int k = 0; k < 3; ++k) // one division site (render.hpp:184)
+                s_cold_d[3 + k][tid] /= survive;
+#else
             tp0 /= survive;
             tp1 /= survive;
             tp2 /= survive;
+#endif
         }
         state = kNeedSegment;
     };
@@ -699,15 +751,28 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         }
         if (state == kNeedPath) {
             if (s == A.spp) {
+#if SVDB_COLD_SHARED
+#pragma unroll 1
+                for (int k = 0; k < 3; ++k) // render.hpp:308-310, one division site
+                    A.out[out_off + k] = float(s_cold_d[k][tid] / double(A.spp));
+#else
                 A.out[out_off] = float(acc0 / double(A.spp));
                 A.out[out_off + 1] = float(acc1 / double(A.spp));
                 A.out[out_off + 2] = float(acc2 / double(A.spp));
+#endif
                 state = kNeedPixel;
                 return;
             }
             rng = Rng::for_pixel_sample(A.seed_mixed, px, py, s);
-            double jx = rng.uniform();
-            double jy = rng.uniform();
+            double jx = 0.0, jy = 0.0;
+#pragma unroll 1
+            for (int k = 0; k < 2; ++k) { // jitter draws (render.hpp:300-301), one generator copy
+                const double u = rng.uniform();
+                if (k == 0)
+                    jx = u;
+                else
+                    jy = u;
+            }
             ray = camera_ray(A.cam, double(px) + jx, double(py) + jy);
             tp0 = tp1 = tp2 = 1.0;
             bounces = 0;
