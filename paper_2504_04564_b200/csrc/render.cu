@@ -579,10 +579,10 @@ struct SharedDda {
 };
 
 #ifndef SVDB_TRACE_THREADS
-#define SVDB_TRACE_THREADS 64 // 2 warps per CTA, <= 96 registers: 20 resident warps per SM
+#define SVDB_TRACE_THREADS 64 // 2 warps per CTA, <= 80 registers: 24 resident warps per SM
 #endif
 #ifndef SVDB_TRACE_MIN_BLOCKS
-#define SVDB_TRACE_MIN_BLOCKS 10
+#define SVDB_TRACE_MIN_BLOCKS 12
 #endif
 #ifndef SVDB_SCHED
 #define SVDB_SCHED 1 // 0: advance-to-point then gather; 1: per-iteration phase selection
