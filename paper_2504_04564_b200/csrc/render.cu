@@ -596,9 +596,6 @@ struct SharedDda {
 #ifndef SVDB_MAJ_AHEAD
 #define SVDB_MAJ_AHEAD 1
 #endif
-#ifndef SVDB_LOCATE_AHEAD
-#define SVDB_LOCATE_AHEAD 0 // measured slower: the extra live registers cost resident warps
-#endif
 #ifndef SVDB_DDA_SHARED
 #define SVDB_DDA_SHARED 1
 #endif
@@ -631,10 +628,6 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
     double t = 0.0, tb = 0.0, inv = 0.0;
 #if SVDB_MAJ_AHEAD
     double inv_ahead = 0.0;
-#endif
-#if SVDB_LOCATE_AHEAD
-    uint4 pend = make_uint4(0, 0, 0, 0);
-    bool pend_ok = false;
 #endif
 #if SVDB_COLD_SHARED
     // Per-lane state touched only at sample start/end, scatter and pixel output lives in shared
@@ -824,17 +817,6 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         }
         t -= log(1.0 - rng.uniform()) * inv;
         state = t >= tb ? kNeedCell : kPoint;
-#if SVDB_LOCATE_AHEAD
-        // software pipelining: a new tentative collision issues the lower-slot load naming its
-        // base voxel's leaf now; the gather (a later iteration) starts with the leaf located
-        if (state == kPoint) {
-            const int x0 = lattice_coord(ray.o[0] + ray.d[0] * t), y0 = lattice_coord(ray.o[1] + ray.d[1] * t),
-                      z0 = lattice_coord(ray.o[2] + ray.d[2] * t);
-            pend_ok = !tr.acc.in_leaf(x0, y0, z0) && tr.acc.in_lower(x0, y0, z0);
-            if (pend_ok)
-                pend = __ldg(A.g.lower + size_t(tr.acc.lower) * 4096 + lower_slot(x0, y0, z0));
-        }
-#endif
     };
     // accept test on the gathered value (render.hpp:119-122) / ratio update
     auto accept = [&](float v) {
@@ -867,18 +849,6 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         float v = float(t * 1e-3 - floor(t * 1e-3));
         ++tr.samples;
 #else
-#if SVDB_LOCATE_AHEAD
-        if (pend_ok && pend.x == kSlotChild) {
-            Accessor<CODEC>& a = tr.acc;
-            a.lx = lattice_coord(ray.o[0] + ray.d[0] * t) & ~7;
-            a.ly = lattice_coord(ray.o[1] + ray.d[1] * t) & ~7;
-            a.lz = lattice_coord(ray.o[2] + ray.d[2] * t) & ~7;
-            a.leaf = pend.y;
-            a.lo = __uint_as_float(pend.z);
-            a.sc = __uint_as_float(pend.w);
-        }
-        pend_ok = false;
-#endif
         float v = tr.sample_at(ray, t);
 #endif
         accept(v);
