@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--kernel", type=int, default=0, help="0 auto (path-regenerating), 1 per-pixel (A/B)")
     ap.add_argument("--mode", default="", help="override the integrator: pathtrace|ratio|ea|iso")
+    ap.add_argument("--majorant-cell", type=int, default=0,
+                    help="majorant grid edge: 0/32 reference macrocells (bit parity), 8 leaf, 128 lower node")
     return ap.parse_args()
 
 
@@ -62,7 +64,7 @@ def scene_for(args):
     from paper_2504_04564_b200 import scenes as S
     sc = S.scaled(args.config, args.scale, image_factor=1) if args.scale > 1 else S.SCENES[args.config]
     import paper_2504_04564_b200 as P
-    st = replace(sc.settings, kernel=args.kernel)
+    st = replace(sc.settings, kernel=args.kernel, majorant_cell=args.majorant_cell)
     if args.spp:
         st = replace(st, spp=args.spp)
     if args.mode:
@@ -341,7 +343,8 @@ def run_ours(args):
         per_launch_lookups = lookups / args.steps / world
         achieved = per_launch_lookups * SECTOR_BYTES / launch_s / 1e9
         traffic, prof = (ncu_traffic(args.config, paths / args.steps / world)
-                         if args.scale == 1 and args.kernel == 0 and not args.mode else (None, None))
+                         if args.scale == 1 and args.kernel == 0 and not args.mode
+                         and args.majorant_cell in (0, 32) else (None, None))
         line = {
             "metric": "Mpaths/s (1024^3 8-bit compressed VDB path tracing; Mlookups/s alongside)",
             "value": value, "unit": "Mpaths/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -350,6 +353,7 @@ def run_ours(args):
             "config": {"workload": f"{sc.name}: {sc.dims[0]}x{sc.dims[1]}x{sc.dims[2]} {sc.volume} -> "
                                    f"{grid.codec.name} leaves, {sc.width}x{sc.height}, {sc.settings.spp} spp, "
                                    f"{sc.settings.mode.name}, max_bounces {sc.settings.max_bounces}",
+                       "majorant_cell": sc.settings.majorant_cell or 32,
                        "image_split": f"interleaved 16x16 tiles over {world} GPU(s), NCCL gather to rank 0",
                        "l2": "inputs larger than L2 (leaf payload "
                              f"{grid.leaf_payload_bytes / 1e9:.2f} GB vs 126 MB L2)",

@@ -89,7 +89,10 @@ typedef struct {
     double ea_min_transmittance; /* EA: early-out threshold (default 1e-4) */
     int32_t tile_rank, tile_nranks; /* image split: 16x16 tiles t with t % nranks == rank */
     int32_t kernel;          /* SVDBGPU_KERNEL_*: 0 auto (path-regenerating tracer), 1 per-pixel */
-    int32_t reserved[3];
+    int32_t majorant_cell;   /* majorant grid cell edge: 0/32 = the reference's 32^3 macrocells
+                                (bit-parity mode); 128 = lower-node, 8 = leaf-node majorants
+                                (node-majorant tracking; statistically equal, different streams) */
+    int32_t reserved[2];
 } svdbgpu_settings;
 
 typedef struct {

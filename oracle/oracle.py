@@ -49,7 +49,8 @@ class _Settings(C.Structure):
                 ("seed", C.c_uint64), ("mode", C.c_int), ("iso_value", C.c_double),
                 ("ambient", C.c_float * 3), ("background", C.c_float * 3),
                 ("ea_step", C.c_double), ("ea_min_transmittance", C.c_double),
-                ("tile_rank", C.c_int), ("tile_nranks", C.c_int), ("threads", C.c_int)]
+                ("tile_rank", C.c_int), ("tile_nranks", C.c_int), ("threads", C.c_int),
+                ("majorant_cell", C.c_int)]
 
 
 def _take_bytes(ptr, n: int) -> bytes:
@@ -199,7 +200,7 @@ class OracleGrid:
                       (C.c_float * 3)(*settings.background_color),
                       getattr(settings, "ea_step", 0.5),
                       getattr(settings, "ea_min_transmittance", 1e-4),
-                      tile_rank, tile_nranks, threads)
+                      tile_rank, tile_nranks, threads, getattr(settings, "majorant_cell", 0))
         if rgb is None:
             rgb = np.zeros((cam.height, cam.width, 3), dtype=np.float32)
         lk = C.c_uint64()

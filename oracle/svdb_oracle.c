@@ -297,24 +297,27 @@ static double tf_max_alpha_in_range(const so_tf* tf, double vlo, double vhi)
 typedef struct {
     int cells[3];
     int dims[3];
+    int cell; /* edge in voxels: 32 = the reference's kMacrocellSize (macrocell.hpp:29); 8/128 =
+                 leaf/lower-node majorant grids (north-star node-majorant mode) */
     float *cmin, *cmax, *maj;
     uint8_t* empty;
 } mc_t;
 
-static inline int cell_count_axis(int d) { int n = (d - 1 + 31) / 32; return n < 1 ? 1 : n; }
+static inline int cell_count_axis(int d, int cd) { int n = (d - 1 + cd - 1) / cd; return n < 1 ? 1 : n; }
 
-static void mc_build(const so_grid* g, const so_tf* tf, mc_t* mc)
+static void mc_build(const so_grid* g, const so_tf* tf, int cd, mc_t* mc)
 {
-    for (int a = 0; a < 3; ++a) { mc->dims[a] = g->dims[a]; mc->cells[a] = cell_count_axis(g->dims[a]); }
+    mc->cell = cd;
+    for (int a = 0; a < 3; ++a) { mc->dims[a] = g->dims[a]; mc->cells[a] = cell_count_axis(g->dims[a], cd); }
     size_t nc = (size_t)mc->cells[0] * mc->cells[1] * mc->cells[2];
     mc->cmin = (float*)malloc(nc * 4); mc->cmax = (float*)malloc(nc * 4);
     mc->maj = (float*)malloc(nc * 4); mc->empty = (uint8_t*)malloc(nc);
     for (size_t i = 0; i < nc; ++i) {
         int cx = (int)(i % mc->cells[0]), cy = (int)((i / mc->cells[0]) % mc->cells[1]),
             cz = (int)(i / ((size_t)mc->cells[0] * mc->cells[1]));
-        int lo[3] = {cx * 32, cy * 32, cz * 32};
+        int lo[3] = {cx * cd, cy * cd, cz * cd};
         int c3[3] = {cx, cy, cz}, hi[3];
-        for (int a = 0; a < 3; ++a) { int h = (c3[a] + 1) * 32; hi[a] = h < g->dims[a] - 1 ? h : g->dims[a] - 1; }
+        for (int a = 0; a < 3; ++a) { int h = (c3[a] + 1) * cd; hi[a] = h < g->dims[a] - 1 ? h : g->dims[a] - 1; }
         acc_t acc = {g, NULL, NULL, NULL, 0};
         float mn = INFINITY, mx = -INFINITY;
         for (int z = lo[2]; z <= hi[2]; ++z)
@@ -346,7 +349,7 @@ int so_macrocells(const so_grid* g, const so_tf* tf, int* cells3, float* cmin, f
                   float* maj, uint8_t* empty, size_t cap)
 {
     mc_t mc;
-    mc_build(g, tf, &mc);
+    mc_build(g, tf, 32, &mc);
     memcpy(cells3, mc.cells, 12);
     size_t nc = (size_t)mc.cells[0] * mc.cells[1] * mc.cells[2];
     if (cmin && nc <= cap) {
@@ -432,22 +435,22 @@ static int dda_init(const mc_t* mc, const ray_t* r, double t0, double t1, dda_t*
     double hi[3] = {(double)(mc->dims[0] - 1), (double)(mc->dims[1] - 1), (double)(mc->dims[2] - 1)};
     if (!clip_ray_box(r, lo, hi, &t0, &t1)) return 0;
     if (!(t0 <= t1)) return 0;
-    double e[3];
+    double e[3], cs = (double)mc->cell;
     ray_at(r, t0, e);
     for (int a = 0; a < 3; ++a) {
-        s->c[a] = (int)dclamp(floor(e[a] / 32.0), 0.0, (double)(mc->cells[a] - 1));
+        s->c[a] = (int)dclamp(floor(e[a] / cs), 0.0, (double)(mc->cells[a] - 1));
         s->step[a] = 0;
         s->t_next[a] = INFINITY;
         s->t_delta[a] = INFINITY;
         double d = r->d[a];
         if (d > 0.0) {
             s->step[a] = 1;
-            s->t_next[a] = ((double)(s->c[a] + 1) * 32.0 - r->o[a]) / d;
-            s->t_delta[a] = 32.0 / d;
+            s->t_next[a] = ((double)(s->c[a] + 1) * cs - r->o[a]) / d;
+            s->t_delta[a] = cs / d;
         } else if (d < 0.0) {
             s->step[a] = -1;
-            s->t_next[a] = ((double)s->c[a] * 32.0 - r->o[a]) / d;
-            s->t_delta[a] = -32.0 / d;
+            s->t_next[a] = ((double)s->c[a] * cs - r->o[a]) / d;
+            s->t_delta[a] = -cs / d;
         }
     }
     s->t_cur = t0;
@@ -804,8 +807,11 @@ int so_render(const so_grid* g, const so_tf* tf, const so_camera* cam, const so_
 {
     if (tf->n_entries < 2 || !(tf->domain_hi > tf->domain_lo)) return E_SIZE;
     if (s->spp < 1 || cam->width < 1 || cam->height < 1) return E_SIZE;
+    int cd = s->majorant_cell;
+    if (cd == 0) cd = 32;
+    if (cd != 8 && cd != 32 && cd != 128) return E_SIZE;
     mc_t mc;
-    mc_build(g, tf, &mc);
+    mc_build(g, tf, cd, &mc);
     int tiles_x = (cam->width + 15) / 16, tiles_y = (cam->height + 15) / 16;
     long total = (long)tiles_x * tiles_y;
     int nr = s->tile_nranks > 0 ? s->tile_nranks : 1;

@@ -51,6 +51,7 @@ typedef struct {
     double ea_min_transmittance; /* EA early termination threshold */
     int tile_rank, tile_nranks;  /* interleaved 16x16 tiles: t % nranks == rank */
     int threads;                 /* 0 = all cores */
+    int majorant_cell;           /* 0/32 reference macrocells; 8 / 128 node-majorant grids */
 } so_settings;
 
 /* SVDB v1 container (io.hpp:22-43); returns 0 or Errc+1 (errors.hpp:11-23). */

@@ -24,7 +24,8 @@ class Settings(C.Structure):
                 ("seed", C.c_uint64), ("mode", C.c_int32), ("iso_value", C.c_double),
                 ("ambient", C.c_float * 3), ("background", C.c_float * 3), ("ea_step", C.c_double),
                 ("ea_min_transmittance", C.c_double), ("tile_rank", C.c_int32),
-                ("tile_nranks", C.c_int32), ("kernel", C.c_int32), ("reserved", C.c_int32 * 3)]
+                ("tile_nranks", C.c_int32), ("kernel", C.c_int32), ("majorant_cell", C.c_int32),
+                ("reserved", C.c_int32 * 2)]
 
 
 class Stats(C.Structure):

@@ -209,13 +209,16 @@ class RenderSettings:
     ea_step: float = 0.5
     ea_min_transmittance: float = 1e-4
     kernel: int = 0  # 0 auto (path-regenerating tracer), 1 per-pixel (A/B); images identical
+    # majorant grid cell edge: 0 = the reference's 32^3 macrocells (bit parity); 128 / 8 =
+    # lower-node / leaf-node majorants (node-majorant tracking, statistically equal)
+    majorant_cell: int = 0
 
     def _c(self, tile_rank: int = 0, tile_nranks: int = 1) -> N.Settings:
         return N.Settings(self.spp, self.max_bounces, self.rr_start_bounce, self.seed, int(self.mode),
                           self.iso_value, (C.c_float * 3)(*self.ambient_radiance),
                           (C.c_float * 3)(*self.background_color), self.ea_step,
                           self.ea_min_transmittance, tile_rank, tile_nranks, self.kernel,
-                          (C.c_int32 * 3)())
+                          self.majorant_cell, (C.c_int32 * 2)())
 
 
 @dataclass

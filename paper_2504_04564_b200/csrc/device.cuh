@@ -432,7 +432,10 @@ struct Dda {
     double t_next[3], t_delta[3], t_cur, t1;
     bool done;
 
-    __device__ __forceinline__ bool init(const int cells[3], const double hi[3], const Ray& r, double t0_, double t1_)
+    // cell = MacrocellGrid::cell_dim (32 in the reference, macrocell.hpp:20) as a double; icell its
+    // exact reciprocal (cell is a power of two, so e * icell == e / cell)
+    __device__ __forceinline__ bool init(const int cells[3], const double hi[3], const Ray& r, double t0_, double t1_,
+                                         double cell, double icell)
     {
         double t0 = t0_;
         t1 = t1_;
@@ -443,19 +446,19 @@ struct Dda {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             double e = r.o[a] + r.d[a] * t0;
-            c[a] = int(dclamp(floor(e / 32.0), 0.0, double(cells[a] - 1)));
+            c[a] = int(dclamp(floor(e * icell), 0.0, double(cells[a] - 1)));
             double d = r.d[a];
             step[a] = 0;
             t_next[a] = __longlong_as_double(0x7ff0000000000000ll);
             t_delta[a] = t_next[a];
             if (d > 0.0) {
                 step[a] = 1;
-                t_next[a] = (double(c[a] + 1) * 32.0 - r.o[a]) / d;
-                t_delta[a] = 32.0 / d;
+                t_next[a] = (double(c[a] + 1) * cell - r.o[a]) / d;
+                t_delta[a] = cell / d;
             } else if (d < 0.0) {
                 step[a] = -1;
-                t_next[a] = (double(c[a]) * 32.0 - r.o[a]) / d;
-                t_delta[a] = -32.0 / d;
+                t_next[a] = (double(c[a]) * cell - r.o[a]) / d;
+                t_delta[a] = -cell / d;
             }
         }
         t_cur = t0;

@@ -249,15 +249,15 @@ __global__ void k_gradient(DevGrid g, const double* __restrict__ xyz, size_t n, 
 
 // ---- K3: exact closed-box ranges, one CTA per 32^3 cell (33^3 voxels incl. shared layer) ----
 template <int CODEC>
-__global__ void __launch_bounds__(256) k_cell_ranges(DevGrid g, int cx_n, int cy_n, float* __restrict__ cmin,
+__global__ void __launch_bounds__(256) k_cell_ranges(DevGrid g, int cx_n, int cy_n, int cd, float* __restrict__ cmin,
                                                      float* __restrict__ cmax)
 {
     const int cell = blockIdx.x;
     const int cx = cell % cx_n, cy = (cell / cx_n) % cy_n, cz = cell / (cx_n * cy_n);
-    const int x0 = cx * 32, y0 = cy * 32, z0 = cz * 32;
-    const int ex = min(x0 + 32, g.dims[0] - 1) - x0 + 1;
-    const int ey = min(y0 + 32, g.dims[1] - 1) - y0 + 1;
-    const int ez = min(z0 + 32, g.dims[2] - 1) - z0 + 1;
+    const int x0 = cx * cd, y0 = cy * cd, z0 = cz * cd;
+    const int ex = min(x0 + cd, g.dims[0] - 1) - x0 + 1;
+    const int ey = min(y0 + cd, g.dims[1] - 1) - y0 + 1;
+    const int ez = min(z0 + cd, g.dims[2] - 1) - z0 + 1;
     Accessor<CODEC> a(g);
     float mn = __int_as_float(0x7f800000), mx = -mn;
     const int total = ex * ey * ez;
@@ -400,22 +400,32 @@ int GridImpl::upload_tf(const svdbgpu_tf* tf, cudaStream_t s, DevTF* out)
     default: F(kCodecAffine4); break;                                                          \
     }
 
-int GridImpl::ensure_ranges(cudaStream_t s, float* ms)
+int GridImpl::ensure_ranges(cudaStream_t s, float* ms, int cd)
 {
-    if (ranges_valid) {
+    if (ranges_valid && cd == cell_dim) {
         if (ms)
             *ms = 0.0f;
         return 0;
     }
-    for (int a = 0; a < 3; ++a)
-        cells[a] = std::max(1, (dg.dims[a] - 1 + 31) / 32); // cell_counts_for (macrocell.hpp:66-70)
+    if (cd != 8 && cd != 32 && cd != 128)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "majorant cell size must be 8, 32 or 128 voxels");
+    cudaFree(d_cmin);
+    cudaFree(d_cmax);
+    cudaFree(d_maj);
+    cudaFree(d_inv_maj);
+    d_cmin = d_cmax = d_maj = nullptr;
+    d_inv_maj = nullptr;
+    ranges_valid = false;
+    cell_dim = cd;
+    for (int a = 0; a < 3; ++a) // cell_counts_for (macrocell.hpp:66-70) with cell_dim cd
+        cells[a] = std::max(1, (dg.dims[a] - 1 + cd - 1) / cd);
     size_t nc = size_t(cells[0]) * cells[1] * cells[2];
     SVDB_CUDA(cudaMalloc(&d_cmin, nc * 4));
     SVDB_CUDA(cudaMalloc(&d_cmax, nc * 4));
     SVDB_CUDA(cudaMalloc(&d_maj, nc * 4));
     SVDB_CUDA(cudaMalloc(&d_inv_maj, nc * 8));
     SVDB_CUDA(cudaEventRecord(ev0, s));
-#define LAUNCH_RANGES(C) k_cell_ranges<C><<<unsigned(nc), 256, 0, s>>>(dg, cells[0], cells[1], d_cmin, d_cmax)
+#define LAUNCH_RANGES(C) k_cell_ranges<C><<<unsigned(nc), 256, 0, s>>>(dg, cells[0], cells[1], cd, d_cmin, d_cmax)
     SVDB_CODEC_DISPATCH(codec, LAUNCH_RANGES)
 #undef LAUNCH_RANGES
     SVDB_CUDA(cudaGetLastError());

@@ -38,7 +38,10 @@ struct GridImpl {
     uint64_t device_bytes = 0, leaf_payload_bytes = 0;
 
     // macrocells: exact closed-box ranges cached per grid (macrocell.hpp:74-103);
-    // majorants recomputed per TF (macrocell.hpp:108-116)
+    // majorants recomputed per TF (macrocell.hpp:108-116). cell_dim 32 is the reference's
+    // (MacrocellGrid::cell_dim); 128 / 8 are the lower-node / leaf-node majorant grids of the
+    // node-majorant tracking mode.
+    int cell_dim = 32;
     int cells[3] = {0, 0, 0};
     float* d_cmin = nullptr;
     float* d_cmax = nullptr;
@@ -57,7 +60,7 @@ struct GridImpl {
     std::mutex mu;
 
     ~GridImpl();
-    int ensure_ranges(cudaStream_t s, float* ms);
+    int ensure_ranges(cudaStream_t s, float* ms, int cell_dim = 32);
     int upload_tf(const svdbgpu_tf* tf, cudaStream_t s, DevTF* out);
 };
 

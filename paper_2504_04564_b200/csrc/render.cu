@@ -36,6 +36,8 @@ struct RenderArgs {
     const float* cmin;
     const float* cmax;
     int cells[3];
+    double cell;  // majorant cell edge in voxels (32 = the reference's MacrocellGrid::cell_dim)
+    double icell; // 1/cell, exact (cell is a power of two), so e * icell == e / cell bit for bit
     double hi[3];
     CamArgs cam;
     int spp, max_bounces, rr_start;
@@ -99,7 +101,7 @@ struct Tracer {
     __device__ __forceinline__ bool next_event(const Ray& r, Rng& rng, double& t_ev, float& v_ev)
     {
         Dda d;
-        if (!d.init(A.cells, A.hi, r, 0.0, kInf()))
+        if (!d.init(A.cells, A.hi, r, 0.0, kInf(), A.cell, A.icell))
             return false;
         int c[3];
         double ta, tb;
@@ -191,7 +193,7 @@ struct Tracer {
             double t_ev = 0.0;
             float v_ev = 0.0f;
             Dda d;
-            if (d.init(A.cells, A.hi, ray, 0.0, kInf())) {
+            if (d.init(A.cells, A.hi, ray, 0.0, kInf(), A.cell, A.icell)) {
                 int c[3];
                 double ta, tb;
                 while (Tr > 0.0 && d.next(A.cells, c, ta, tb)) {
@@ -261,7 +263,7 @@ struct Tracer {
                 int c[3];
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
-                    c[a] = int(dclamp(floor(p[a] / 32.0), 0.0, double(A.cells[a] - 1)));
+                    c[a] = int(dclamp(floor(p[a] * A.icell), 0.0, double(A.cells[a] - 1)));
                 if (__ldg(A.maj + cell_index(c)) == 0.0f) {
                     // exact skip: find this empty cell's exit along the ray and resume at the
                     // last sample index before it (the per-sample test handles the rest)
@@ -269,9 +271,9 @@ struct Tracer {
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
                         if (ray.d[a] > 0.0)
-                            te = dmin(te, (double(c[a] + 1) * 32.0 - ray.o[a]) / ray.d[a]);
+                            te = dmin(te, (double(c[a] + 1) * A.cell - ray.o[a]) / ray.d[a]);
                         else if (ray.d[a] < 0.0)
-                            te = dmin(te, (double(c[a]) * 32.0 - ray.o[a]) / ray.d[a]);
+                            te = dmin(te, (double(c[a]) * A.cell - ray.o[a]) / ray.d[a]);
                     }
                     double kk = floor((te - t0) / dt - j) - 1.0;
                     if (kk > double(k))
@@ -303,7 +305,7 @@ struct Tracer {
         bool hit = false;
         double hit_t = 0.0;
         Dda d;
-        if (d.init(A.cells, A.hi, ray, 0.0, kInf())) {
+        if (d.init(A.cells, A.hi, ray, 0.0, kInf(), A.cell, A.icell)) {
             int c[3];
             double ta, tb;
             while (!hit && d.next(A.cells, c, ta, tb)) {
@@ -495,7 +497,8 @@ struct SharedDda {
     // clip_ray_box + dda_traverse setup (dda.hpp:25-86). Rolled per-axis loops keep one copy of
     // each FP64 division in the instruction stream (this runs once per flight segment); the
     // operations and their order per axis are exactly the reference's.
-    __device__ __forceinline__ bool init(const int cells[3], const double hi[3], const Ray& r, double t0, double t1)
+    __device__ __forceinline__ bool init(const int cells[3], const double hi[3], const Ray& r, double t0, double t1,
+                                         double cell, double icell)
     {
 #pragma unroll 1
         for (int a = 0; a < 3; ++a) {
@@ -527,13 +530,13 @@ struct SharedDda {
             const double d = a == 0 ? r.d[0] : (a == 1 ? r.d[1] : r.d[2]);
             const int n = a == 0 ? cells[0] : (a == 1 ? cells[1] : cells[2]);
             const double e = o + d * t0;
-            const int c = int(dclamp(floor(e / 32.0), 0.0, double(n - 1)));
+            const int c = int(dclamp(floor(e * icell), 0.0, double(n - 1)));
             int step = 0;
             double tn = __longlong_as_double(0x7ff0000000000000ll), td = tn;
             if (d != 0.0) {
                 step = d > 0.0 ? 1 : -1;
-                tn = (double(d > 0.0 ? c + 1 : c) * 32.0 - o) / d;
-                td = (d > 0.0 ? 32.0 : -32.0) / d;
+                tn = (double(d > 0.0 ? c + 1 : c) * cell - o) / d;
+                td = (d > 0.0 ? cell : -cell) / d;
             }
             ci(a) = c;
             ci(3 + a) = step;
@@ -778,7 +781,7 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             Tr = 1.0;
             have = false;
         }
-        if (!dda.init(A.cells, A.hi, ray, 0.0, kInf())) {
+        if (!dda.init(A.cells, A.hi, ray, 0.0, kInf(), A.cell, A.icell)) {
             end_segment();
             return;
         }
@@ -1040,7 +1043,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     if (int rc = g->upload_tf(tf, s, &A.tf))
         return rc;
     float range_ms = 0.0f;
-    if (int rc = g->ensure_ranges(s, &range_ms))
+    if (int rc = g->ensure_ranges(s, &range_ms, st->majorant_cell > 0 ? st->majorant_cell : 32))
         return rc;
     SVDB_CUDA(cudaEventRecord(g->ev0, s));
     if (int rc = majorants(g, A.tf, s))
@@ -1056,6 +1059,8 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     A.cmax = g->d_cmax;
     for (int a = 0; a < 3; ++a) {
         A.cells[a] = g->cells[a];
+        A.cell = double(g->cell_dim);
+        A.icell = 1.0 / A.cell;
         A.hi[a] = double(g->dg.dims[a] - 1); // world box [0, dims-1] (macrocell.hpp:50-54)
     }
     host_camera(cam, &A.cam);

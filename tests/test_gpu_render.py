@@ -107,6 +107,43 @@ def test_ratio_and_delta_agree_statistically(gpu):
     assert abs(a.mean() - b.mean()) < 0.01 * max(b.mean(), 1e-3) + 3e-3
 
 
+@pytest.mark.parametrize("cell", [8, 128])
+@pytest.mark.parametrize("mode", [P.RenderMode.pathtrace, P.RenderMode.ratio])
+def test_node_majorant_grid_matches_oracle(gpu, orc, cell, mode):
+    # leaf / lower-node majorant grids: same streams as the oracle at the same cell size
+    sc = S.scaled("C3", 16, spp=4, image_factor=8, mode=mode)
+    st = P.RenderSettings(spp=4, seed=5, max_bounces=64, rr_start_bounce=3, mode=mode, majorant_cell=cell)
+    _, svdb, _ = scene_svdb(sc)
+    g = P.DeviceGrid(svdb, P.Codec.affine8)
+    deq, _, _ = orc.quantize(svdb, int(P.Codec.affine8))
+    og = orc.open(deq)
+    img, (want, lookups, _) = _render_pair(lambda tf, cam, s: og.render(tf, cam, s), g, sc, st)
+    same, rmse = image_parity(img.pixels, want)
+    print(f"cell {cell} {mode.name}: identical {same:.4f} rmse {rmse:.2e}")
+    assert rmse <= RMSE_TOL and same >= 0.98
+    if mode == P.RenderMode.pathtrace:
+        assert abs(img.stats["lookups"] - lookups) <= 1e-3 * lookups
+
+
+def test_node_majorant_grid_is_unbiased_at_scale(gpu):
+    # 256^3 turbulence: 8^3 / 128^3 majorant grids vs the reference's 32^3 macrocells, image means
+    sc = S.scaled("C3", 4, spp=16, image_factor=8)
+    _, svdb, _ = scene_svdb(sc)
+    g = P.DeviceGrid(svdb, P.Codec.affine8)
+    cam = sc.camera()
+    means = {}
+    for cell in (32, 8, 128):
+        st = P.RenderSettings(spp=16, seed=21, max_bounces=64, rr_start_bounce=3, majorant_cell=cell)
+        img = P.render(g, sc.tf, cam, st)
+        means[cell] = (img.pixels.mean(), img.stats["lookups"])
+    print(means)
+    for cell in (8, 128):
+        assert abs(means[cell][0] - means[32][0]) < 3e-3
+    assert means[8][1] < means[32][1]
+    with pytest.raises(P.Error):
+        P.render(g, sc.tf, cam, P.RenderSettings(spp=1, majorant_cell=16))
+
+
 def test_tile_split_is_bit_identical(gpu):
     # GPU-count invariance (test_render.cpp:296-322 pins thread counts the same way):
     # interleaved tiles rendered as 3 "ranks" and reassembled equal the 1-rank frame bit for bit

@@ -165,6 +165,24 @@ def test_ratio_and_delta_estimators_agree_in_homogeneous_cube(orc, ref):
     assert r.std() <= d.std() * 1.05  # ratio tracking never noisier here
 
 
+@pytest.mark.parametrize("cell", [8, 128])
+def test_node_majorant_grids_are_unbiased(orc, cell):
+    # delta tracking is unbiased for any bounding majorant: leaf (8^3) and lower-node (128^3)
+    # majorant grids estimate the same image as the reference's 32^3 macrocells, with fewer
+    # lookups for the tighter grid
+    sc = S.scaled("C3", 16, spp=32, image_factor=16)
+    _, svdb, _ = scene_svdb(sc)
+    og = orc.open(svdb)
+    cam = sc.camera()
+    base, lk32, _ = og.render(sc.tf, cam, P.RenderSettings(spp=32, seed=1, max_bounces=64, rr_start_bounce=3))
+    img, lk, _ = og.render(sc.tf, cam, P.RenderSettings(spp=32, seed=1, max_bounces=64, rr_start_bounce=3,
+                                                         majorant_cell=cell))
+    assert abs(img.mean() - base.mean()) < 3e-3
+    assert (lk < lk32) if cell == 8 else (lk >= lk32)
+    with pytest.raises(RuntimeError):
+        og.render(sc.tf, cam, P.RenderSettings(spp=1, majorant_cell=16))
+
+
 def test_ea_transmittance_is_beer_lambert(orc, ref):
     # EA through a homogeneous slab: T = exp(-sigma * L) up to the dt discretisation (exact here:
     # a = 1 - exp(-sigma dt) compounds to exp(-sigma * n dt))
