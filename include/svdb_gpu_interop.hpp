@@ -78,19 +78,53 @@ inline Grid upload(const svdb::FrozenGrid& g, Codec codec = Codec::f32, int devi
     throw svdb::Error(svdb::Errc::io_error, "unreachable");
 }
 
-/// Per-process cache: one device grid per FrozenGrid address (frames re-render the same grid).
+/// Per-process cache: one device grid per FrozenGrid (frames re-render the same grid). Entries are
+/// keyed by address and codec and validated by a fingerprint of the grid's shape and storage
+/// (dims, background, node counts, vector data pointers, first/last leaf values), so a different
+/// grid later constructed at the same address is re-uploaded instead of served stale. FrozenGrid
+/// is immutable by contract (frozen.hpp:225-227); in-place edits of leaf values are not detected.
 class GridCache {
 public:
     static Grid& get(const svdb::FrozenGrid& g, Codec codec)
     {
+        struct Entry {
+            std::vector<uint64_t> fp;
+            std::unique_ptr<Grid> grid;
+        };
         static std::mutex mu;
-        static std::map<std::pair<const svdb::FrozenGrid*, int>, std::unique_ptr<Grid>> cache;
+        static std::map<std::pair<const svdb::FrozenGrid*, int>, Entry> cache;
         std::lock_guard<std::mutex> lk(mu);
+        std::vector<uint64_t> fp = fingerprint(g);
         auto key = std::make_pair(&g, int(codec));
         auto it = cache.find(key);
+        if (it != cache.end() && it->second.fp != fp) {
+            cache.erase(it);
+            it = cache.end();
+        }
         if (it == cache.end())
-            it = cache.emplace(key, std::make_unique<Grid>(upload(g, codec))).first;
-        return *it->second;
+            it = cache.emplace(key, Entry{fp, std::make_unique<Grid>(upload(g, codec))}).first;
+        return *it->second.grid;
+    }
+
+private:
+    static std::vector<uint64_t> fingerprint(const svdb::FrozenGrid& g)
+    {
+        auto bits = [](float f) {
+            uint32_t u;
+            std::memcpy(&u, &f, 4);
+            return uint64_t(u);
+        };
+        std::vector<uint64_t> fp = {uint64_t(uint32_t(g.dims.x)), uint64_t(uint32_t(g.dims.y)),
+                                    uint64_t(uint32_t(g.dims.z)), bits(g.background),
+                                    g.root.size(), g.uppers.size(), g.lowers.size(), g.leaves.size(),
+                                    uint64_t(reinterpret_cast<uintptr_t>(g.uppers.data())),
+                                    uint64_t(reinterpret_cast<uintptr_t>(g.lowers.data())),
+                                    uint64_t(reinterpret_cast<uintptr_t>(g.leaves.data()))};
+        if (!g.leaves.empty()) {
+            fp.push_back(bits(g.leaves.front().values.front()));
+            fp.push_back(bits(g.leaves.back().values.back()));
+        }
+        return fp;
     }
 };
 

@@ -92,6 +92,85 @@ int main()
         report("sample_bit_exact", ok);
     }
 
+    // 5. acceptance criterion 6 (acceptance.cpp:169-199) through the GPU sampler: a lossless grid
+    //    sampled at 1e5 random positions equals a dense trilinear oracle within 1e-6
+    {
+        DenseVolume v = synth_blobs({64, 64, 64}, 31, 7);
+        auto [g6, r6] = compress(v, CompressionParams{});
+        gpu::Grid dg = gpu::upload(g6, gpu::Codec::f32);
+        Rng rng(606);
+        std::vector<gpu::Vec3d> pts(100000);
+        for (auto& p : pts)
+            p = {rng.uniform() * 80.0 - 8.0, rng.uniform() * 80.0 - 8.0, rng.uniform() * 80.0 - 8.0};
+        std::vector<float> got = gpu::sample(dg, pts, gpu::SampleMode::trilinear);
+        auto dense_read = [&](const Coord& p) -> double {
+            return v.contains(p) ? double(v.at(p)) : double(g6.background);
+        };
+        double worst = 0.0;
+        for (size_t i = 0; i < pts.size(); ++i) {
+            const auto& p = pts[i];
+            int x0 = int(std::floor(p[0])), y0 = int(std::floor(p[1])), z0 = int(std::floor(p[2]));
+            double fx = p[0] - x0, fy = p[1] - y0, fz = p[2] - z0, want = 0.0;
+            for (int dz = 0; dz < 2; ++dz)
+                for (int dy = 0; dy < 2; ++dy)
+                    for (int dx = 0; dx < 2; ++dx)
+                        want += (dx ? fx : 1 - fx) * (dy ? fy : 1 - fy) * (dz ? fz : 1 - fz) *
+                                dense_read({x0 + dx, y0 + dy, z0 + dz});
+            worst = std::max(worst, std::abs(double(got[i]) - want));
+        }
+        char buf[64];
+        std::snprintf(buf, sizeof buf, "worst %.2e", worst);
+        report("acceptance6_sampler_oracle", worst <= 1e-6, buf);
+    }
+
+    // 6. acceptance criterion 12 (acceptance.cpp:483-529): repeat renders identical, and the GPU
+    //    frame equals the reference's render_field with a dense-sampler substitution
+    {
+        DenseVolume v = synth_blobs({64, 64, 64}, 17, 7);
+        auto [g12, r12] = compress(v, CompressionParams{});
+        TransferFunction tf12(0.0, double(v.max_value()), {{{0.3f, 0.7f, 0.9f, 0.0f}}, {{0.9f, 0.5f, 0.2f, 0.85f}}},
+                              3.0);
+        MacrocellGrid mc = build_macrocells(g12);
+        update_majorants(mc, tf12);
+        Camera c12;
+        c12.position = {20.0, 45.0, -110.0};
+        c12.look_at = {31.5, 31.5, 31.5};
+        c12.width = 128;
+        c12.height = 128;
+        RenderSettings r;
+        r.spp = 16;
+        r.seed = 4096;
+        Image one = gpu::render(g12, tf12, c12, r);
+        Image two = gpu::render(g12, tf12, c12, r);
+        struct DenseReader {
+            const DenseVolume* v;
+            float background;
+            float operator()(const Coord& p) const { return v->contains(p) ? v->at(p) : background; }
+        };
+        Image dense = render_field(DenseReader{&v, g12.background}, mc, tf12, c12, r);
+        size_t rep_same = 0, dense_same = 0;
+        for (size_t i = 0; i < one.pixels.size(); ++i) {
+            rep_same += std::memcmp(&one.pixels[i], &two.pixels[i], sizeof(Vec3f)) == 0;
+            dense_same += std::memcmp(&one.pixels[i], &dense.pixels[i], sizeof(Vec3f)) == 0;
+        }
+        char buf[96];
+        std::snprintf(buf, sizeof buf, "repeat %zu/%zu dense %zu/%zu", rep_same, one.pixels.size(), dense_same,
+                      one.pixels.size());
+        report("acceptance12_determinism_dense_substitution",
+               rep_same == one.pixels.size() && dense_same >= one.pixels.size() * 98 / 100, buf);
+    }
+
+    // 7. GridCache: a different grid at the same address is re-uploaded, not served stale
+    {
+        auto* slot = new FrozenGrid(compress(synth_blobs({32, 32, 32}, 5, 3), CompressionParams{}).first);
+        float a = gpu::sample(*slot, Vec3d{16.25, 16.5, 16.75}, SampleMode::trilinear);
+        *slot = compress(synth_blobs({40, 40, 40}, 6, 4), CompressionParams{}).first;
+        float b = gpu::sample(*slot, Vec3d{16.25, 16.5, 16.75}, SampleMode::trilinear);
+        Accessor acc(*slot);
+        report("grid_cache_revalidates", b == sample(acc, Vec3d{16.25, 16.5, 16.75}, SampleMode::trilinear) && a != b);
+        delete slot;
+    }
+
     // 4. error mapping: corrupt containers raise the reference's Errc
     {
         std::vector<uint8_t> bytes = serialize_frozen(grid);
