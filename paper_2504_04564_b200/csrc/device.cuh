@@ -263,11 +263,45 @@ __device__ __forceinline__ int apron_offset(int r, int x, int y, int z)
 
 // One tap of the 9^3 stencil brick of the cached leaf: own block or apron, decoded with the
 // owning block's parameters. All eight taps of a sample are independent loads.
+#ifndef SVDB_BRANCHLESS_TAP
+#define SVDB_BRANCHLESS_TAP 1
+#endif
 template <int CODEC>
 __device__ __forceinline__ double brick_tap(const Accessor<CODEC>& a, int x, int y, int z)
 {
     const uint8_t* base = a.g->codes + size_t(a.leaf) * a.g->leaf_stride;
     const int r = (x >> 3) | ((y >> 3) << 1) | ((z >> 3) << 2);
+#if SVDB_BRANCHLESS_TAP
+    // Same element as the region switch below, from per-region coefficient tables, so lanes whose
+    // taps fall in different regions do not diverge: own block (r = 0) x + 8y + 64z; apron region
+    // r packs its remaining axes x-fastest with stride 8 after the 512 own elements.
+    const int xr = x & 7, yr = y & 7, zr = z & 7;
+    const int cy = (0x00180018u >> (4 * r)) & 15;
+    const int cz = (0x01080840u >> (8 * r)) & 255;
+    const int ab = int((0xD8D0C880C0400000ull >> (8 * r)) & 255);
+    const int off = ((~r) & 1) * xr + cy * yr + cz * zr; // element within own block / region
+    if constexpr (CODEC == kCodecF32) {
+        const int e = r ? 512 + ab + off : off;
+        return double(__ldg(reinterpret_cast<const float*>(base) + e));
+    } else {
+        float lo = a.lo, sc = a.sc;
+        if constexpr (CODEC != kCodecUnorm8) {
+            if (r) {
+                const float2 p = __ldg(a.g->lparams + size_t(a.leaf) * 8 + r);
+                lo = p.x;
+                sc = p.y;
+            }
+        }
+        if constexpr (CODEC == kCodecAffine4) { // own: packed nibbles; apron: one code per byte
+            const int bi = r ? 256 + ab + off : off >> 1;
+            const int sh = r ? 0 : (off & 1) * 4;
+            return double(decode_code<CODEC>((uint32_t(__ldg(base + bi)) >> sh) & 15u, lo, sc));
+        } else {
+            const int e = r ? 512 + ab + off : off;
+            return double(decode_code<CODEC>(__ldg(base + e), lo, sc));
+        }
+    }
+#endif
     if (r == 0)
         return double(decode<CODEC>(*a.g, a.leaf, x + 8 * (y + 8 * z), a.lo, a.sc));
     const int e = apron_offset(r, x & 7, y & 7, z & 7);

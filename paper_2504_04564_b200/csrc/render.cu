@@ -602,6 +602,12 @@ struct SharedDda {
 #ifndef SVDB_DDA_SHARED
 #define SVDB_DDA_SHARED 1
 #endif
+#ifndef SVDB_RAY_SHARED
+#define SVDB_RAY_SHARED 1
+#endif
+#ifndef SVDB_ACC_SHARED
+#define SVDB_ACC_SHARED 1
+#endif
 template <int CODEC, int MODE>
 __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
 {
@@ -616,7 +622,51 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
 
     Tracer<CODEC> tr(A, s_ent);
     Rng rng{0};
+#if SVDB_RAY_SHARED
+    // the flight's ray is read only by the gather and written only at path start / scatter:
+    // kept in shared memory (SoA) so the advance loop does not hold its 12 registers
+    __shared__ double s_ray[6][SVDB_TRACE_THREADS];
+    auto ray_load = [&]() {
+        Ray r;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            r.o[k] = reinterpret_cast<volatile double*>(s_ray[k])[threadIdx.x];
+            r.d[k] = reinterpret_cast<volatile double*>(s_ray[3 + k])[threadIdx.x];
+        }
+        return r;
+    };
+    auto ray_store = [&](const Ray& r) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            reinterpret_cast<volatile double*>(s_ray[k])[threadIdx.x] = r.o[k];
+            reinterpret_cast<volatile double*>(s_ray[3 + k])[threadIdx.x] = r.d[k];
+        }
+    };
+#else
     Ray ray;
+    auto ray_load = [&]() { return ray; };
+    auto ray_store = [&](const Ray& r) { ray = r; };
+#endif
+#if SVDB_ACC_SHARED
+    // the accessor's node caches (frozen.hpp:228-277) are used only by the gather: shared memory
+    // between gathers, registers inside one
+    __shared__ int s_acc[14][SVDB_TRACE_THREADS];
+    auto acc_io = [&](bool store) {
+        volatile int* p = &s_acc[0][threadIdx.x];
+        int* f[14] = {&tr.acc.lx, &tr.acc.ly, &tr.acc.lz, reinterpret_cast<int*>(&tr.acc.leaf),
+                      reinterpret_cast<int*>(&tr.acc.lo), reinterpret_cast<int*>(&tr.acc.sc),
+                      &tr.acc.wx, &tr.acc.wy, &tr.acc.wz, reinterpret_cast<int*>(&tr.acc.lower),
+                      &tr.acc.ux, &tr.acc.uy, &tr.acc.uz, &tr.acc.upper};
+#pragma unroll
+        for (int k = 0; k < 14; ++k) {
+            if (store)
+                p[k * SVDB_TRACE_THREADS] = *f[k];
+            else
+                *f[k] = p[k * SVDB_TRACE_THREADS];
+        }
+    };
+    acc_io(true);
+#endif
 #if SVDB_DDA_SHARED
     __shared__ int s_dda_i[7][SVDB_TRACE_THREADS];
     __shared__ double s_dda_d[8][SVDB_TRACE_THREADS];
@@ -635,17 +685,20 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
 #if SVDB_COLD_SHARED
     // Per-lane state touched only at sample start/end, scatter and pixel output lives in shared
     // memory (SoA, conflict-free), keeping the step/gather loop's register footprint small.
-    __shared__ double s_cold_d[13][SVDB_TRACE_THREADS];
+    __shared__ double s_cold_d[7][SVDB_TRACE_THREADS];
+    __shared__ double s_ratio_d[RATIO ? 5 : 1][SVDB_TRACE_THREADS]; // ratio tracking only
     __shared__ int s_cold_i[6][SVDB_TRACE_THREADS];
     const int tid = threadIdx.x;
     volatile double &acc0 = s_cold_d[0][tid], &acc1 = s_cold_d[1][tid], &acc2 = s_cold_d[2][tid];
     volatile double &tp0 = s_cold_d[3][tid], &tp1 = s_cold_d[4][tid], &tp2 = s_cold_d[5][tid];
-    volatile double &L0 = s_cold_d[6][tid], &L1 = s_cold_d[7][tid], &L2 = s_cold_d[8][tid];
-    volatile double &Tr = s_cold_d[9][tid], &t_ev = s_cold_d[10][tid];
+    volatile double& t_ev = s_cold_d[6][tid];
+    constexpr int kR = RATIO ? 1 : 0; // pathtrace: the ratio names alias one unused row
+    volatile double &L0 = s_ratio_d[0][tid], &L1 = s_ratio_d[kR][tid], &L2 = s_ratio_d[2 * kR][tid];
+    volatile double &Tr = s_ratio_d[3 * kR][tid];
+    volatile double& have_d = s_ratio_d[4 * kR][tid]; // ratio: event pending (0/1)
     volatile int &px = s_cold_i[0][tid], &py = s_cold_i[1][tid], &s = s_cold_i[2][tid];
     volatile int &bounces = s_cold_i[3][tid], &out_off = s_cold_i[4][tid];
     volatile float& v_ev = reinterpret_cast<volatile float&>(s_cold_i[5][tid]);
-    volatile double& have_d = s_cold_d[11][tid]; // ratio: event pending (0/1)
     struct HaveRef {
         volatile double& d;
         __device__ operator bool() const { return d != 0.0; }
@@ -697,10 +750,14 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         tp0 = tpv[0];
         tp1 = tpv[1];
         tp2 = tpv[2];
-        ray.o[0] = ray.o[0] + ray.d[0] * te;
-        ray.o[1] = ray.o[1] + ray.d[1] * te;
-        ray.o[2] = ray.o[2] + ray.d[2] * te;
-        tr.isotropic(rng, ray.d);
+        {
+            Ray ray = ray_load();
+            ray.o[0] = ray.o[0] + ray.d[0] * te;
+            ray.o[1] = ray.o[1] + ray.d[1] * te;
+            ray.o[2] = ray.o[2] + ray.d[2] * te;
+            tr.isotropic(rng, ray.d);
+            ray_store(ray);
+        }
         if (bounces >= A.rr_start) {
             double survive = dclamp(dmax(tp0, dmax(tp1, tp2)), 0.05, 0.95);
             if (rng.uniform() >= survive) {
@@ -769,7 +826,7 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
                 else
                     jy = u;
             }
-            ray = camera_ray(A.cam, double(px) + jx, double(py) + jy);
+            ray_store(camera_ray(A.cam, double(px) + jx, double(py) + jy));
             tp0 = tp1 = tp2 = 1.0;
             bounces = 0;
             if constexpr (RATIO)
@@ -781,7 +838,7 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             Tr = 1.0;
             have = false;
         }
-        if (!dda.init(A.cells, A.hi, ray, 0.0, kInf(), A.cell, A.icell)) {
+        if (!dda.init(A.cells, A.hi, ray_load(), 0.0, kInf(), A.cell, A.icell)) {
             end_segment();
             return;
         }
@@ -852,7 +909,13 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         float v = float(t * 1e-3 - floor(t * 1e-3));
         ++tr.samples;
 #else
-        float v = tr.sample_at(ray, t);
+#if SVDB_ACC_SHARED
+        acc_io(false);
+#endif
+        float v = tr.sample_at(ray_load(), t);
+#if SVDB_ACC_SHARED
+        acc_io(true);
+#endif
 #endif
         accept(v);
     };
