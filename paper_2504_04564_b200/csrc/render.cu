@@ -593,6 +593,19 @@ struct SharedDda {
 #ifndef SVDB_W_SAMPLE
 #define SVDB_W_SAMPLE 1
 #endif
+#ifndef SVDB_ADV_ITERS
+#define SVDB_ADV_ITERS 3 // advance steps per advance-phase invocation
+#endif
+#ifndef SVDB_GATHER_ADV
+#define SVDB_GATHER_ADV 0
+#endif
+#ifndef SVDB_ADV_FRAC
+#define SVDB_ADV_FRAC 0 // > 0: stop early once fewer than nA / FRAC lanes still advance
+#endif
+#ifndef SVDB_W_START_NUM
+#define SVDB_W_START_NUM 1
+#define SVDB_W_START_DEN 1
+#endif
 #ifndef SVDB_COLD_SHARED
 #define SVDB_COLD_SHARED 1
 #endif
@@ -970,7 +983,9 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             const int nS = __popc(__ballot_sync(live, state == kPoint));
             const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell));
             const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter));
-            const int phase = (nS * SVDB_W_SAMPLE >= nA && nS * SVDB_W_SAMPLE >= nT) ? 2 : (nA >= nT ? 1 : 0);
+            // start lanes may wait to batch up, but a non-empty phase is always chosen
+            const int nTw = nT > 0 ? max(1, nT * SVDB_W_START_NUM / SVDB_W_START_DEN) : 0;
+            const int phase = (nS * SVDB_W_SAMPLE >= nA && nS * SVDB_W_SAMPLE >= nTw) ? 2 : (nA >= nTw ? 1 : 0);
 #ifdef SVDB_PHASE_STATS
             if (lane == __ffs(live) - 1) { // per phase: invocations and participating lanes
                 const int n = phase == 0 ? nT : (phase == 1 ? nA : nS);
@@ -986,10 +1001,26 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
                 if (state == kNeedPath || state == kNeedSegment || state == kScatter)
                     do_start();
             } else if (phase == 1) {
-                if (state == kNeedCell || state == kInCell)
+#if SVDB_ADV_FRAC
+                // keep advancing while enough of the phase's lanes are still advancing
+                for (int k = 0;; ++k) {
+                    const bool adv = state == kNeedCell || state == kInCell;
+                    const int n = __popc(__ballot_sync(live, adv));
+                    if (n == 0 || k >= SVDB_ADV_ITERS || n * SVDB_ADV_FRAC < nA)
+                        break;
+                    if (adv)
+                        do_advance();
+                }
+#else
+#pragma unroll 1
+                for (int k = 0; k < SVDB_ADV_ITERS && (state == kNeedCell || state == kInCell); ++k)
                     do_advance();
+#endif
             } else if (state == kPoint) {
                 do_sample();
+#pragma unroll 1
+                for (int k = 0; k < SVDB_GATHER_ADV && (state == kNeedCell || state == kInCell); ++k)
+                    do_advance(); // rejected collisions draw their next step at once
             }
 #ifdef SVDB_PHASE_STATS
             __syncwarp(live);
