@@ -692,6 +692,9 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
     auto dda_done = [&]() { return dda.done; };
 #endif
     double t = 0.0, tb = 0.0, inv = 0.0;
+#ifdef SVDB_PHASE_STATS
+    unsigned st_empty = 0, st_full = 0;
+#endif
 #if SVDB_MAJ_AHEAD
     double inv_ahead = 0.0;
 #endif
@@ -883,7 +886,10 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
 #else
             inv = __ldg(A.inv_maj + tr.cell_index(c));
 #endif
-            if (inv == 0.0)
+#ifdef SVDB_PHASE_STATS
+            ++(inv > 0.0 ? st_full : st_empty);
+#endif
+            if (!(inv > 0.0))
                 return;
             t = ta;
             tb = tbb;
@@ -1047,6 +1053,10 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         s64 += __shfl_xor_sync(FULL, s64, off);
     if (lane == 0 && s64)
         atomicAdd(A.counters, s64);
+#ifdef SVDB_PHASE_STATS
+    atomicAdd(A.counters + 12, (unsigned long long)st_empty); // macrocell visits: empty / non-empty
+    atomicAdd(A.counters + 13, (unsigned long long)st_full);
+#endif
 }
 
 __global__ void k_unpack(const float* __restrict__ packed, int nranks, long long max_tiles, int w, int h, int tiles_x,
@@ -1231,6 +1241,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         unsigned long long c[16];
         cudaMemcpy(c, g->d_counters, 128, cudaMemcpyDeviceToHost);
         const char* names[3] = {"start", "advance", "gather"};
+        fprintf(stderr, "[phase-stats] macrocell visits: empty %llu non-empty %llu\n", c[12], c[13]);
         for (int p = 0; p < 3; ++p)
             fprintf(stderr, "[phase-stats] %-8s invocations %llu lanes/invocation %.2f cycles/invocation %.1f\n",
                     names[p], c[2 + 2 * p], c[2 + 2 * p] ? double(c[3 + 2 * p]) / double(c[2 + 2 * p]) : 0.0,
