@@ -593,6 +593,12 @@ struct SharedDda {
 #ifndef SVDB_W_SAMPLE
 #define SVDB_W_SAMPLE 1
 #endif
+#ifndef SVDB_SPEC_LOG
+#define SVDB_SPEC_LOG 1
+#endif
+#ifndef SVDB_FAST_EXIT
+#define SVDB_FAST_EXIT 0
+#endif
 #ifndef SVDB_ADV_ITERS
 #define SVDB_ADV_ITERS 3 // advance steps per advance-phase invocation
 #endif
@@ -866,6 +872,12 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
     // kNeedCell -> next macrocell (empty cells draw nothing, render.hpp:145-146);
     // kInCell -> one tentative step t -= ln(1-u)/sigma_maj (render.hpp:116-118)
     auto do_advance = [&]() {
+#if SVDB_SPEC_LOG
+        // the step draw's log does not depend on the DDA: compute it from the next uniform before
+        // the cell lookup (independent FP64 chains interleave); the draw is consumed only if the
+        // cell has draws, so the stream is unchanged
+        const double lg = log(1.0 - rng.peek());
+#endif
         if (state == kNeedCell) {
             int c[3];
             double ta, tbb;
@@ -894,7 +906,27 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             t = ta;
             tb = tbb;
         }
+#if SVDB_FAST_EXIT
+        // Most draws leave the cell, and then only the decision t_new >= tb is used, never t_new.
+        // Decide it from a float lower bound of -ln(w) (MUFU lg2: |error| <= 4e-7 (1 + y), bound
+        // taken 10x wider) when the bound already clears the gap; the FP64 log runs only for
+        // collisions and near-ties, so every decision and collision point equals the exact path's.
+        const double w = 1.0 - rng.uniform(); // exact: u is a multiple of 2^-53
+        {
+            const float y = -__log2f(float(w)) * 0.693147182f;
+            const float y_lb = y - (4e-6f + 4e-6f * y);
+            if (y_lb * float(inv) * 0.999999f > float(tb - t) * 1.000001f) {
+                state = kNeedCell;
+                return;
+            }
+        }
+        t -= log(w) * inv;
+#elif SVDB_SPEC_LOG
+        rng.skip();
+        t -= lg * inv;
+#else
         t -= log(1.0 - rng.uniform()) * inv;
+#endif
         state = t >= tb ? kNeedCell : kPoint;
     };
     // accept test on the gathered value (render.hpp:119-122) / ratio update
