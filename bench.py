@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--kernel", type=int, default=0, help="0 auto (path-regenerating), 1 per-pixel (A/B)")
     ap.add_argument("--mode", default="", help="override the integrator: pathtrace|ratio|ea|iso")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
+                    help="tracking arithmetic: fp64 reference-exact (bit parity), fp32 (tolerance parity)")
     ap.add_argument("--majorant-cell", type=int, default=0,
                     help="majorant grid edge: 0/32 reference macrocells (bit parity), 8 leaf, 128 lower node")
     return ap.parse_args()
@@ -66,7 +68,8 @@ def scene_for(args):
     from paper_2504_04564_b200 import scenes as S
     sc = S.scaled(args.config, args.scale, image_factor=1) if args.scale > 1 else S.SCENES[args.config]
     import paper_2504_04564_b200 as P
-    st = replace(sc.settings, kernel=args.kernel, majorant_cell=args.majorant_cell)
+    st = replace(sc.settings, kernel=args.kernel, majorant_cell=args.majorant_cell,
+                 precision=1 if args.precision == "fp32" else 0)
     if args.spp:
         st = replace(st, spp=args.spp)
     if args.mode:
@@ -361,12 +364,12 @@ def run_ours(args):
         achieved = per_launch_lookups * SECTOR_BYTES / launch_s / 1e9
         traffic, prof = (ncu_traffic(args.config, paths / args.steps / world)
                          if args.scale == 1 and args.kernel == 0 and not args.mode
-                         and args.majorant_cell in (0, 32) else (None, None))
+                         and args.majorant_cell in (0, 32) and args.precision == "fp64" else (None, None))
         line = {
             "metric": "Mpaths/s (1024^3 8-bit compressed VDB path tracing; Mlookups/s alongside)",
             "value": value, "unit": "Mpaths/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32" if sc.settings.precision else "f64", "data": "synthetic",
             "config": {"workload": f"{sc.name}: {sc.dims[0]}x{sc.dims[1]}x{sc.dims[2]} {sc.volume} -> "
                                    f"{grid.codec.name} leaves, {sc.width}x{sc.height}, {sc.settings.spp} spp, "
                                    f"{sc.settings.mode.name}, max_bounces {sc.settings.max_bounces}",

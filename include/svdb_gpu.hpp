@@ -124,6 +124,8 @@ struct RenderSettings {
     double ea_step = 0.5;
     double ea_min_transmittance = 1e-4;
     int tile_rank = 0, tile_nranks = 1;
+    int majorant_cell = 0; // 0/32 reference macrocells; 8 / 128 node-majorant grids
+    int precision = 0;     // SVDBGPU_PRECISION_FP64 (bit parity) / SVDBGPU_PRECISION_FP32
 
     svdbgpu_settings c() const
     {
@@ -142,6 +144,8 @@ struct RenderSettings {
         s.ea_min_transmittance = ea_min_transmittance;
         s.tile_rank = tile_rank;
         s.tile_nranks = tile_nranks;
+        s.majorant_cell = majorant_cell;
+        s.precision = precision;
         return s;
     }
 };

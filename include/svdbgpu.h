@@ -58,6 +58,11 @@ enum {
     SVDBGPU_MODE_RATIO = 3      /* multi-scatter path, ratio-tracked escape transmittance */
 };
 
+/* Tracking arithmetic. FP64 reproduces the reference bit for bit (render.hpp is FP64); FP32 keeps
+   the reference's algorithm and per-pixel draw order in single precision, matching its images
+   within the north-star tolerance (relative RMSE <= 1e-3 at matched streams and spp). */
+enum { SVDBGPU_PRECISION_FP64 = 0, SVDBGPU_PRECISION_FP32 = 1 };
+
 /* Kernel variants for A/B measurement; both produce bit-identical images. */
 enum { SVDBGPU_KERNEL_AUTO = 0, SVDBGPU_KERNEL_PER_PIXEL = 1 };
 
@@ -92,7 +97,8 @@ typedef struct {
     int32_t majorant_cell;   /* majorant grid cell edge: 0/32 = the reference's 32^3 macrocells
                                 (bit-parity mode); 128 = lower-node, 8 = leaf-node majorants
                                 (node-majorant tracking; statistically equal, different streams) */
-    int32_t reserved[2];
+    int32_t precision;       /* SVDBGPU_PRECISION_*: tracking arithmetic (pathtrace / ratio) */
+    int32_t reserved[1];
 } svdbgpu_settings;
 
 typedef struct {

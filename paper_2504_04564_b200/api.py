@@ -212,13 +212,16 @@ class RenderSettings:
     # majorant grid cell edge: 0 = the reference's 32^3 macrocells (bit parity); 128 / 8 =
     # lower-node / leaf-node majorants (node-majorant tracking, statistically equal)
     majorant_cell: int = 0
+    # tracking arithmetic: 0 = FP64 reference-exact (bit parity), 1 = FP32 (images within the
+    # north-star tolerance at matched streams; pathtrace / ratio only)
+    precision: int = 0
 
     def _c(self, tile_rank: int = 0, tile_nranks: int = 1) -> N.Settings:
         return N.Settings(self.spp, self.max_bounces, self.rr_start_bounce, self.seed, int(self.mode),
                           self.iso_value, (C.c_float * 3)(*self.ambient_radiance),
                           (C.c_float * 3)(*self.background_color), self.ea_step,
                           self.ea_min_transmittance, tile_rank, tile_nranks, self.kernel,
-                          self.majorant_cell, (C.c_int32 * 2)())
+                          self.majorant_cell, self.precision, (C.c_int32 * 1)())
 
 
 @dataclass

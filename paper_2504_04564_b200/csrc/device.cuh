@@ -267,7 +267,7 @@ __device__ __forceinline__ int apron_offset(int r, int x, int y, int z)
 #define SVDB_BRANCHLESS_TAP 1
 #endif
 template <int CODEC>
-__device__ __forceinline__ double brick_tap(const Accessor<CODEC>& a, int x, int y, int z)
+__device__ __forceinline__ float brick_tap_f(const Accessor<CODEC>& a, int x, int y, int z)
 {
     const uint8_t* base = a.g->codes + size_t(a.leaf) * a.g->leaf_stride;
     const int r = (x >> 3) | ((y >> 3) << 1) | ((z >> 3) << 2);
@@ -282,7 +282,7 @@ __device__ __forceinline__ double brick_tap(const Accessor<CODEC>& a, int x, int
     const int off = ((~r) & 1) * xr + cy * yr + cz * zr; // element within own block / region
     if constexpr (CODEC == kCodecF32) {
         const int e = r ? 512 + ab + off : off;
-        return double(__ldg(reinterpret_cast<const float*>(base) + e));
+        return __ldg(reinterpret_cast<const float*>(base) + e);
     } else {
         float lo = a.lo, sc = a.sc;
         if constexpr (CODEC != kCodecUnorm8) {
@@ -295,22 +295,29 @@ __device__ __forceinline__ double brick_tap(const Accessor<CODEC>& a, int x, int
         if constexpr (CODEC == kCodecAffine4) { // own: packed nibbles; apron: one code per byte
             const int bi = r ? 256 + ab + off : off >> 1;
             const int sh = r ? 0 : (off & 1) * 4;
-            return double(decode_code<CODEC>((uint32_t(__ldg(base + bi)) >> sh) & 15u, lo, sc));
+            return decode_code<CODEC>((uint32_t(__ldg(base + bi)) >> sh) & 15u, lo, sc);
         } else {
             const int e = r ? 512 + ab + off : off;
-            return double(decode_code<CODEC>(__ldg(base + e), lo, sc));
+            return decode_code<CODEC>(__ldg(base + e), lo, sc);
         }
     }
-#endif
+#else
     if (r == 0)
-        return double(decode<CODEC>(*a.g, a.leaf, x + 8 * (y + 8 * z), a.lo, a.sc));
+        return decode<CODEC>(*a.g, a.leaf, x + 8 * (y + 8 * z), a.lo, a.sc);
     const int e = apron_offset(r, x & 7, y & 7, z & 7);
     if constexpr (CODEC == kCodecF32) {
-        return double(__ldg(reinterpret_cast<const float*>(base + a.g->main_bytes) + e));
+        return __ldg(reinterpret_cast<const float*>(base + a.g->main_bytes) + e);
     } else {
         const float2 p = __ldg(a.g->lparams + size_t(a.leaf) * 8 + r);
-        return double(decode_code<CODEC>(__ldg(base + a.g->main_bytes + e), p.x, p.y));
+        return decode_code<CODEC>(__ldg(base + a.g->main_bytes + e), p.x, p.y);
     }
+#endif
+}
+
+template <int CODEC>
+__device__ __forceinline__ double brick_tap(const Accessor<CODEC>& a, int x, int y, int z)
+{
+    return double(brick_tap_f<CODEC>(a, x, y, z));
 }
 
 template <int CODEC>

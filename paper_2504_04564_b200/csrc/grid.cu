@@ -296,7 +296,8 @@ __global__ void __launch_bounds__(256) k_cell_ranges(DevGrid g, int cx_n, int cy
 
 __global__ void k_majorants(DevTF tf, const float4* __restrict__ ent_g, const float* __restrict__ cmin,
                             const float* __restrict__ cmax, int n, float* __restrict__ maj,
-                            double* __restrict__ inv_maj, uint8_t* __restrict__ empty)
+                            double* __restrict__ inv_maj, float* __restrict__ inv_maj_f,
+                            uint8_t* __restrict__ empty)
 {
     extern __shared__ float4 ent[];
     for (int i = threadIdx.x; i < tf.n; i += blockDim.x)
@@ -310,6 +311,7 @@ __global__ void k_majorants(DevTF tf, const float4* __restrict__ ent_g, const fl
     // woodcock_track's inv_maj = 1.0 / sigma_maj with sigma_maj = double(float majorant)
     // (render.hpp:113, 147); 0 marks "no draws here" (empty or zero float majorant)
     inv_maj[i] = float(m) > 0.0f ? 1.0 / double(float(m)) : 0.0;
+    inv_maj_f[i] = float(inv_maj[i]);
     if (empty)
         empty[i] = m == 0.0 ? 1 : 0;
 }
@@ -345,6 +347,7 @@ GridImpl::~GridImpl()
     cudaFree(d_cmax);
     cudaFree(d_maj);
     cudaFree(d_inv_maj);
+    cudaFree(d_inv_maj_f);
     cudaFree(d_tf);
     cudaFree(d_img);
     cudaFree(d_counters);
@@ -413,8 +416,10 @@ int GridImpl::ensure_ranges(cudaStream_t s, float* ms, int cd)
     cudaFree(d_cmax);
     cudaFree(d_maj);
     cudaFree(d_inv_maj);
+    cudaFree(d_inv_maj_f);
     d_cmin = d_cmax = d_maj = nullptr;
     d_inv_maj = nullptr;
+    d_inv_maj_f = nullptr;
     ranges_valid = false;
     cell_dim = cd;
     for (int a = 0; a < 3; ++a) // cell_counts_for (macrocell.hpp:66-70) with cell_dim cd
@@ -424,6 +429,7 @@ int GridImpl::ensure_ranges(cudaStream_t s, float* ms, int cd)
     SVDB_CUDA(cudaMalloc(&d_cmax, nc * 4));
     SVDB_CUDA(cudaMalloc(&d_maj, nc * 4));
     SVDB_CUDA(cudaMalloc(&d_inv_maj, nc * 8));
+    SVDB_CUDA(cudaMalloc(&d_inv_maj_f, nc * 4));
     SVDB_CUDA(cudaEventRecord(ev0, s));
 #define LAUNCH_RANGES(C) k_cell_ranges<C><<<unsigned(nc), 256, 0, s>>>(dg, cells[0], cells[1], cd, d_cmin, d_cmax)
     SVDB_CODEC_DISPATCH(codec, LAUNCH_RANGES)
@@ -443,7 +449,7 @@ int majorants(GridImpl* g, const DevTF& tf, cudaStream_t s, uint8_t* d_empty)
 {
     int nc = g->cells[0] * g->cells[1] * g->cells[2];
     k_majorants<<<(nc + 255) / 256, 256, sizeof(float4) * size_t(tf.n), s>>>(tf, g->d_tf, g->d_cmin, g->d_cmax, nc,
-                                                                            g->d_maj, g->d_inv_maj, d_empty);
+                                                                            g->d_maj, g->d_inv_maj, g->d_inv_maj_f, d_empty);
     SVDB_CUDA(cudaGetLastError());
     return 0;
 }

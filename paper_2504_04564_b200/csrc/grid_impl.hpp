@@ -47,6 +47,7 @@ struct GridImpl {
     float* d_cmax = nullptr;
     float* d_maj = nullptr;
     double* d_inv_maj = nullptr; // 1.0 / double(majorant), 0 for empty cells
+    float* d_inv_maj_f = nullptr; // the same in float (FP32 tracking kernel)
     bool ranges_valid = false;
     float4* d_tf = nullptr;
     int tf_cap = 0;

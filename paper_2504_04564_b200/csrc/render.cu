@@ -12,6 +12,7 @@
 //   trace_iso     render.hpp:193-255   -> trace_iso
 #include "device.cuh"
 #include "grid_impl.hpp"
+#include "render_args.hpp"
 
 #include <cmath>
 #include <cstdio>
@@ -20,36 +21,6 @@
 namespace svdbgpu {
 
 namespace {
-
-struct CamArgs {
-    double pos[3], fwd[3], right[3], up[3];
-    double tan_half, aspect;
-    int w, h;
-};
-
-struct RenderArgs {
-    DevGrid g;
-    DevTF tf;
-    const float4* tf_ent;
-    const float* maj;
-    const double* inv_maj;
-    const float* cmin;
-    const float* cmax;
-    int cells[3];
-    double cell;  // majorant cell edge in voxels (32 = the reference's MacrocellGrid::cell_dim)
-    double icell; // 1/cell, exact (cell is a power of two), so e * icell == e / cell bit for bit
-    double hi[3];
-    CamArgs cam;
-    int spp, max_bounces, rr_start;
-    uint64_t seed_mixed;
-    double iso;
-    float ambient[3], background[3];
-    double ea_step, ea_min_t;
-    int rank, nranks, tiles_x;
-    float* out;
-    int packed;
-    unsigned long long* counters;
-};
 
 constexpr double kPi = 3.14159265358979323846;
 
@@ -1174,6 +1145,13 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         return fail_code(SVDBGPU_E_INVALID_ARG, "tile_rank out of range");
     if (st->mode == SVDBGPU_MODE_EA && !(st->ea_step > 0.0))
         return fail_code(SVDBGPU_E_INVALID_ARG, "ea_step must be positive");
+    if (st->precision != SVDBGPU_PRECISION_FP64 && st->precision != SVDBGPU_PRECISION_FP32)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "unknown precision");
+    const bool fp32 = st->precision == SVDBGPU_PRECISION_FP32;
+    if (fp32 && (st->kernel == SVDBGPU_KERNEL_PER_PIXEL ||
+                 (st->mode != SVDBGPU_MODE_PATHTRACE && st->mode != SVDBGPU_MODE_RATIO)))
+        return fail_code(SVDBGPU_E_UNSUPPORTED, "FP32 tracking is implemented for the pathtrace and ratio "
+                                                "integrators of the path-regenerating kernel");
     SVDB_CUDA(cudaSetDevice(g->device));
     RenderArgs A{};
     if (int rc = g->upload_tf(tf, s, &A.tf))
@@ -1191,6 +1169,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     A.tf_ent = g->d_tf;
     A.maj = g->d_maj;
     A.inv_maj = g->d_inv_maj;
+    A.inv_maj_f = g->d_inv_maj_f;
     A.cmin = g->d_cmin;
     A.cmax = g->d_cmax;
     for (int a = 0; a < 3; ++a) {
@@ -1249,7 +1228,9 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         if (wave) LAUNCH_T(C, SVDBGPU_MODE_RATIO) else LAUNCH_R(C, SVDBGPU_MODE_RATIO);         \
         break;                                                                                 \
     }
-        switch (g->codec) {
+        if (fp32)
+            launch_trace_fast(A, g->codec, st->mode, n_units, smem, s);
+        else switch (g->codec) {
         case kCodecF32: BY_MODE(kCodecF32) break;
         case kCodecUnorm8: BY_MODE(kCodecUnorm8) break;
         case kCodecAffine8: BY_MODE(kCodecAffine8) break;

@@ -1,0 +1,46 @@
+// render_args.hpp — launch arguments shared by the FP64 reference-exact kernels (render.cu) and
+// the FP32 tracking kernel (render_fast.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "layout.hpp"
+
+namespace svdbgpu {
+
+struct CamArgs {
+    double pos[3], fwd[3], right[3], up[3];
+    double tan_half, aspect;
+    int w, h;
+};
+
+struct RenderArgs {
+    DevGrid g;
+    DevTF tf;
+    const float4* tf_ent;
+    const float* maj;
+    const double* inv_maj;
+    const float* inv_maj_f; // float(1 / majorant), 0 for cells without draws (FP32 tracking)
+    const float* cmin;
+    const float* cmax;
+    int cells[3];
+    double cell;  // majorant cell edge in voxels (32 = the reference's MacrocellGrid::cell_dim)
+    double icell; // 1/cell, exact (cell is a power of two), so e * icell == e / cell bit for bit
+    double hi[3];
+    CamArgs cam;
+    int spp, max_bounces, rr_start;
+    uint64_t seed_mixed;
+    double iso;
+    float ambient[3], background[3];
+    double ea_step, ea_min_t;
+    int rank, nranks, tiles_x;
+    float* out;
+    int packed;
+    unsigned long long* counters;
+};
+
+// FP32 tracking kernel launch (render_fast.cu): persistent grid sized from occupancy.
+int launch_trace_fast(const RenderArgs& A, int codec, int mode, long long n_units, size_t smem, cudaStream_t s);
+
+} // namespace svdbgpu
