@@ -50,9 +50,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the mixed-precision side measurement")
     ap.add_argument("--kernel", type=int, default=0, help="0 auto (path-regenerating), 1 per-pixel (A/B)")
     ap.add_argument("--mode", default="", help="override the integrator: pathtrace|ratio|ea|iso")
-    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32", "mixed"],
                     help="tracking arithmetic: fp64 reference-exact (bit parity), fp32 (tolerance parity)")
     ap.add_argument("--majorant-cell", type=int, default=0,
                     help="majorant grid edge: 0/32 reference macrocells (bit parity), 8 leaf, 128 lower node")
@@ -69,7 +70,7 @@ def scene_for(args):
     sc = S.scaled(args.config, args.scale, image_factor=1) if args.scale > 1 else S.SCENES[args.config]
     import paper_2504_04564_b200 as P
     st = replace(sc.settings, kernel=args.kernel, majorant_cell=args.majorant_cell,
-                 precision=1 if args.precision == "fp32" else 0)
+                 precision={"fp64": 0, "fp32": 1, "mixed": 2}[args.precision])
     if args.spp:
         st = replace(st, spp=args.spp)
     if args.mode:
@@ -323,6 +324,41 @@ def run_ours(args):
     else:
         render_max = sum(render_ms)
 
+    # ---- the mixed-precision tracking variant of the same workload (precision=2: FP64 geometry,
+    # FP32 step / sampler / TF arithmetic), timed the same way, and its distance to the FP64 frame
+    # at matched streams (north-star tolerance: relative RMSE <= 1e-3) ----
+    fp32 = None
+    if world == 1 and not args.no_fp32 and sc.settings.precision == 0 and args.kernel == 0 and \
+            sc.settings.mode in (P.RenderMode.pathtrace, P.RenderMode.ratio):
+        from dataclasses import replace as _replace
+        ref_frame = frame.clone()
+        st32 = _replace(sc.settings, precision=2)
+        P.render_device(grid, sc.tf, cam, st32, frame.data_ptr(), stream.cuda_stream)
+        torch.cuda.synchronize(dev)
+        d = (frame.double() - ref_frame.double())
+        rel_rmse = float(torch.sqrt((d * d).sum() / (ref_frame.double() ** 2).sum().clamp_min(1e-300)))
+        k32 = max(1, min(args.steps, 3))
+        ms32 = 0.0
+        n32 = l32 = 0
+        for _ in range(k32):
+            if flush_l2:
+                with torch.cuda.stream(stream):
+                    flush.fill_(0.0)
+            ev0.record(stream)
+            st = P.render_device(grid, sc.tf, cam, st32, frame.data_ptr(), stream.cuda_stream)
+            ev1.record(stream)
+            ev1.synchronize()
+            ms32 += ev0.elapsed_time(ev1)
+            n32 += st["paths"]
+            l32 += st["lookups"]
+        fp32 = {"value": n32 / (ms32 / 1e3) / 1e6, "unit": "Mpaths/s", "steps": k32,
+                "mlookups_per_s": l32 / (ms32 / 1e3) / 1e6,
+                "roofline_frac": l32 * SECTOR_BYTES / (ms32 / 1e3) / 1e9 / peaks()[0],
+                "rel_rmse_vs_fp64": rel_rmse, "dtype": "f64/f32",
+                "note": "same workload with SVDBGPU_PRECISION_MIXED (FP64 ray/DDA/distances, FP32 step log, "
+                        "sampler weights, TF, throughput); image compared with the FP64 frame above at "
+                        "matched streams (north-star tolerance 1e-3)"}
+
     # ---- e2e through the C-ABI host-buffer call (svdbgpu_render): H2D of the TF, D2H image ----
     e2e = None
     if not args.no_e2e:
@@ -369,7 +405,7 @@ def run_ours(args):
             "metric": "Mpaths/s (1024^3 8-bit compressed VDB path tracing; Mlookups/s alongside)",
             "value": value, "unit": "Mpaths/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32" if sc.settings.precision else "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": ["f64", "f32", "f64/f32"][sc.settings.precision], "data": "synthetic",
             "config": {"workload": f"{sc.name}: {sc.dims[0]}x{sc.dims[1]}x{sc.dims[2]} {sc.volume} -> "
                                    f"{grid.codec.name} leaves, {sc.width}x{sc.height}, {sc.settings.spp} spp, "
                                    f"{sc.settings.mode.name}, max_bounces {sc.settings.max_bounces}",
@@ -397,6 +433,8 @@ def run_ours(args):
         }
         if e2e:
             line["e2e"] = e2e
+        if fp32:
+            line["mixed_precision_tracking"] = fp32
         if world == 1 and not args.no_cpu_baseline:
             try:
                 cb = cpu_reference_sample(sc, svdb, int(grid.codec), args.cpu_seconds)

@@ -58,10 +58,12 @@ enum {
     SVDBGPU_MODE_RATIO = 3      /* multi-scatter path, ratio-tracked escape transmittance */
 };
 
-/* Tracking arithmetic. FP64 reproduces the reference bit for bit (render.hpp is FP64); FP32 keeps
-   the reference's algorithm and per-pixel draw order in single precision, matching its images
-   within the north-star tolerance (relative RMSE <= 1e-3 at matched streams and spp). */
-enum { SVDBGPU_PRECISION_FP64 = 0, SVDBGPU_PRECISION_FP32 = 1 };
+/* Tracking arithmetic. FP64 reproduces the reference bit for bit (render.hpp is FP64). The other
+   two keep the reference's algorithm and per-pixel draw order: FP32 runs everything in single
+   precision; MIXED keeps ray origins/directions, distances and the DDA in FP64 and runs the step
+   log, uniforms, transfer function, trilinear weights and throughput in FP32. Both match the
+   reference images within a tolerance instead of bit for bit. */
+enum { SVDBGPU_PRECISION_FP64 = 0, SVDBGPU_PRECISION_FP32 = 1, SVDBGPU_PRECISION_MIXED = 2 };
 
 /* Kernel variants for A/B measurement; both produce bit-identical images. */
 enum { SVDBGPU_KERNEL_AUTO = 0, SVDBGPU_KERNEL_PER_PIXEL = 1 };

@@ -212,8 +212,9 @@ class RenderSettings:
     # majorant grid cell edge: 0 = the reference's 32^3 macrocells (bit parity); 128 / 8 =
     # lower-node / leaf-node majorants (node-majorant tracking, statistically equal)
     majorant_cell: int = 0
-    # tracking arithmetic: 0 = FP64 reference-exact (bit parity), 1 = FP32 (images within the
-    # north-star tolerance at matched streams; pathtrace / ratio only)
+    # tracking arithmetic (pathtrace / ratio): 0 = FP64 reference-exact (bit parity); 2 = mixed
+    # (FP64 ray / DDA / distances, FP32 step log, sampler, TF, throughput) and 1 = all FP32, both
+    # matching the FP64 image within a tolerance at matched streams
     precision: int = 0
 
     def _c(self, tile_rank: int = 0, tile_nranks: int = 1) -> N.Settings:

@@ -1145,9 +1145,9 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         return fail_code(SVDBGPU_E_INVALID_ARG, "tile_rank out of range");
     if (st->mode == SVDBGPU_MODE_EA && !(st->ea_step > 0.0))
         return fail_code(SVDBGPU_E_INVALID_ARG, "ea_step must be positive");
-    if (st->precision != SVDBGPU_PRECISION_FP64 && st->precision != SVDBGPU_PRECISION_FP32)
+    if (st->precision < SVDBGPU_PRECISION_FP64 || st->precision > SVDBGPU_PRECISION_MIXED)
         return fail_code(SVDBGPU_E_INVALID_ARG, "unknown precision");
-    const bool fp32 = st->precision == SVDBGPU_PRECISION_FP32;
+    const bool fp32 = st->precision != SVDBGPU_PRECISION_FP64;
     if (fp32 && (st->kernel == SVDBGPU_KERNEL_PER_PIXEL ||
                  (st->mode != SVDBGPU_MODE_PATHTRACE && st->mode != SVDBGPU_MODE_RATIO)))
         return fail_code(SVDBGPU_E_UNSUPPORTED, "FP32 tracking is implemented for the pathtrace and ratio "
@@ -1229,7 +1229,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         break;                                                                                 \
     }
         if (fp32)
-            launch_trace_fast(A, g->codec, st->mode, n_units, smem, s);
+            launch_trace_fast(A, g->codec, st->mode, st->precision, n_units, smem, s);
         else switch (g->codec) {
         case kCodecF32: BY_MODE(kCodecF32) break;
         case kCodecUnorm8: BY_MODE(kCodecUnorm8) break;

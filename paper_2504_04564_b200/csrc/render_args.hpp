@@ -40,7 +40,10 @@ struct RenderArgs {
     unsigned long long* counters;
 };
 
-// FP32 tracking kernel launch (render_fast.cu): persistent grid sized from occupancy.
-int launch_trace_fast(const RenderArgs& A, int codec, int mode, long long n_units, size_t smem, cudaStream_t s);
+// FP32-arithmetic tracking kernel launch (render_fast.cu): SVDBGPU_PRECISION_FP32 (all FP32) or
+// SVDBGPU_PRECISION_MIXED (FP64 ray / DDA / distances, FP32 for the rest); persistent grid sized
+// from occupancy.
+int launch_trace_fast(const RenderArgs& A, int codec, int mode, int precision, long long n_units, size_t smem,
+                      cudaStream_t s);
 
 } // namespace svdbgpu

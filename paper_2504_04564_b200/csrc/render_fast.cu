@@ -21,20 +21,31 @@
 #include "svdbgpu.h"
 
 #include <algorithm>
+#include <type_traits>
+
+#ifndef SVDB_MIX_ACCEPT64
+#define SVDB_MIX_ACCEPT64 0
+#endif
+#ifndef SVDB_MIX_SAMPLE64
+#define SVDB_MIX_SAMPLE64 0
+#endif
 
 namespace svdbgpu {
 
 namespace {
 
 constexpr int kT = 64;          // threads per CTA
-constexpr int kMinBlocks = 16;  // 32 warps per SM
+constexpr int kMinBlocks = 16;  // 32 warps per SM (pure FP32)
+constexpr int kMinBlocksMixed = 12; // FP64 geometry: 264 B of shared state per lane
 constexpr int kAdvIters = 3;    // advance steps per advance-phase invocation
 constexpr unsigned kFull = 0xffffffffu;
 
 enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4, kPoint = 5, kScatter = 6 };
 
-struct RayF {
-    float o[3], d[3];
+// geometry type G: float (pure FP32) or double (FP64 ray / DDA / t, FP32 everything else)
+template <typename G>
+struct RayG {
+    G o[3], d[3];
 };
 
 // splitmix64 uniform (rng.hpp:54-63) truncated to 24 bits: the float just below the double draw
@@ -54,10 +65,24 @@ struct RngF {
         return u24(state);
     }
     __device__ __forceinline__ float peek() const { return u24(state + 0x9E3779B97F4A7C15ull); }
+    __device__ __forceinline__ double uniform53() // the reference's draw (rng.hpp:54-63)
+    {
+        state += 0x9E3779B97F4A7C15ull;
+        uint64_t x = state;
+        x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+        x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+        x ^= x >> 31;
+        return double(x >> 11) * 0x1.0p-53;
+    }
     __device__ __forceinline__ void skip() { state += 0x9E3779B97F4A7C15ull; }
 };
 
-__device__ __forceinline__ float kInfF() { return __int_as_float(0x7f800000); }
+template <typename G>
+__device__ __forceinline__ G kInfG() { return G(__int_as_float(0x7f800000)); }
+template <typename G>
+__device__ __forceinline__ G gmin(G a, G b) { return b < a ? b : a; }
+template <typename G>
+__device__ __forceinline__ G gmax(G a, G b) { return a < b ? b : a; }
 
 // transfer.hpp:47-67 in float; lo / 1/(hi-lo) / scale converted once per launch
 struct TfF {
@@ -87,19 +112,20 @@ struct TfF {
     }
 };
 
-__device__ __forceinline__ int lattice_coord_f(float v)
+template <typename G>
+__device__ __forceinline__ int lattice_coord_g(G f) // f = floor(v)
 {
-    const float f = floorf(v);
-    return f < -1.0e9f ? -1000000000 : (f > 1.0e9f ? 1000000000 : int(f));
+    return f < G(-1.0e9) ? -1000000000 : (f > G(1.0e9) ? 1000000000 : int(f));
 }
 
 // sample_trilinear (sample.hpp:46-72) with float weights; taps through the apron brick as in the
 // FP64 sampler (device.cuh), per-tap accessor reads when the base voxel is not in a leaf
-template <int CODEC>
-__device__ __forceinline__ float sample_f(Accessor<CODEC>& a, float px, float py, float pz)
+template <int CODEC, typename G>
+__device__ __forceinline__ float sample_f(Accessor<CODEC>& a, G px, G py, G pz)
 {
-    const int x0 = lattice_coord_f(px), y0 = lattice_coord_f(py), z0 = lattice_coord_f(pz);
-    const float wx = px - floorf(px), wy = py - floorf(py), wz = pz - floorf(pz);
+    const G fx = floor(px), fy = floor(py), fz = floor(pz);
+    const int x0 = lattice_coord_g(fx), y0 = lattice_coord_g(fy), z0 = lattice_coord_g(fz);
+    const float wx = float(px - fx), wy = float(py - fy), wz = float(pz - fz);
     float v[8];
     float c0;
     if (a.locate(x0, y0, z0, c0)) {
@@ -120,54 +146,56 @@ __device__ __forceinline__ float sample_f(Accessor<CODEC>& a, float px, float py
 }
 
 // camera_ray (render.hpp:259-269) from the host-exact basis
-__device__ __forceinline__ RayF camera_ray_f(const CamArgs& c, float px, float py)
+template <typename G>
+__device__ __forceinline__ RayG<G> camera_ray_g(const CamArgs& c, G px, G py)
 {
-    const float ndc_x = (2.0f * px / float(c.w) - 1.0f) * float(c.tan_half * c.aspect);
-    const float ndc_y = (1.0f - 2.0f * py / float(c.h)) * float(c.tan_half);
-    RayF r;
-    float d[3];
+    const G ndc_x = (G(2) * px / G(c.w) - G(1)) * G(c.tan_half) * G(c.aspect);
+    const G ndc_y = (G(1) - G(2) * py / G(c.h)) * G(c.tan_half);
+    RayG<G> r;
+    G d[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        r.o[a] = float(c.pos[a]);
-        d[a] = float(c.fwd[a]) + float(c.right[a]) * ndc_x + float(c.up[a]) * ndc_y;
+        r.o[a] = G(c.pos[a]);
+        d[a] = G(c.fwd[a]) + G(c.right[a]) * ndc_x + G(c.up[a]) * ndc_y;
     }
-    const float il = rsqrtf(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    const G len = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
 #pragma unroll
     for (int a = 0; a < 3; ++a)
-        r.d[a] = d[a] * il;
+        r.d[a] = d[a] / len;
     return r;
 }
 
 // Macrocell DDA (dda.hpp:25-109) in float, per-lane state in shared memory (SoA)
-struct SharedDdaF {
-    volatile int* si;   // [7][kT]: c0..2, step0..2, done
-    volatile float* sf; // [8][kT]: t_next0..2, t_delta0..2, t_cur, t1
+template <typename G>
+struct SharedDdaG {
+    volatile int* si; // [7][kT]: c0..2, step0..2, done
+    volatile G* sf;   // [8][kT]: t_next0..2, t_delta0..2, t_cur, t1
     int tid;
     __device__ __forceinline__ volatile int& ci(int k) { return si[k * kT + tid]; }
-    __device__ __forceinline__ volatile float& cf(int k) { return sf[k * kT + tid]; }
+    __device__ __forceinline__ volatile G& cf(int k) { return sf[k * kT + tid]; }
     __device__ __forceinline__ bool done() { return ci(6) != 0; }
     __device__ __forceinline__ int index(const int cells[3]) { return ci(0) + cells[0] * (ci(1) + cells[1] * ci(2)); }
 
-    __device__ __forceinline__ bool init(const int cells[3], const float hi[3], const RayF& r, float cell, float icell)
+    __device__ __forceinline__ bool init(const int cells[3], const G hi[3], const RayG<G>& r, G cell, G icell)
     {
-        float t0 = 0.0f, t1 = kInfF();
+        G t0 = G(0), t1 = kInfG<G>();
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const float o = r.o[a], d = r.d[a];
-            if (d == 0.0f) {
-                if (o < 0.0f || o > hi[a])
+            const G o = r.o[a], d = r.d[a];
+            if (d == G(0)) {
+                if (o < G(0) || o > hi[a])
                     return false;
                 continue;
             }
-            const float inv = 1.0f / d;
-            float ta = (0.0f - o) * inv, tb = (hi[a] - o) * inv;
+            const G inv = G(1) / d;
+            G ta = (G(0) - o) * inv, tb = (hi[a] - o) * inv;
             if (ta > tb) {
-                const float tt = ta;
+                const G tt = ta;
                 ta = tb;
                 tb = tt;
             }
-            t0 = fmaxf(t0, ta);
-            t1 = fminf(t1, tb);
+            t0 = gmax(t0, ta);
+            t1 = gmin(t1, tb);
             if (t0 > t1)
                 return false;
         }
@@ -175,14 +203,14 @@ struct SharedDdaF {
             return false;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const float o = r.o[a], d = r.d[a];
-            const int c = int(fminf(fmaxf(floorf((o + d * t0) * icell), 0.0f), float(cells[a] - 1)));
+            const G o = r.o[a], d = r.d[a];
+            const int c = int(gmin(gmax(G(floor((o + d * t0) * icell)), G(0)), G(cells[a] - 1)));
             int step = 0;
-            float tn = kInfF(), td = kInfF();
-            if (d != 0.0f) {
-                step = d > 0.0f ? 1 : -1;
-                tn = (float(d > 0.0f ? c + 1 : c) * cell - o) / d;
-                td = (d > 0.0f ? cell : -cell) / d;
+            G tn = kInfG<G>(), td = kInfG<G>();
+            if (d != G(0)) {
+                step = d > G(0) ? 1 : -1;
+                tn = (G(d > G(0) ? c + 1 : c) * cell - o) / d;
+                td = (d > G(0) ? cell : -cell) / d;
             }
             ci(a) = c;
             ci(3 + a) = step;
@@ -195,16 +223,16 @@ struct SharedDdaF {
         return true;
     }
 
-    __device__ __forceinline__ bool next(const int cells[3], float& ta, float& tb)
+    __device__ __forceinline__ bool next(const int cells[3], G& ta, G& tb)
     {
         if (ci(6))
             return false;
-        const float n0 = cf(0), n1 = cf(1), n2 = cf(2), t_cur = cf(6), t1 = cf(7);
+        const G n0 = cf(0), n1 = cf(1), n2 = cf(2), t_cur = cf(6), t1 = cf(7);
         const bool ax1 = n1 < n0;
-        const float tm = ax1 ? n1 : n0;
+        const G tm = ax1 ? n1 : n0;
         const bool ax2 = n2 < tm;
         const int axis = ax2 ? 2 : (ax1 ? 1 : 0);
-        const float t_exit = fmaxf(fminf(ax2 ? n2 : tm, t1), t_cur);
+        const G t_exit = gmax(gmin(ax2 ? n2 : tm, t1), t_cur);
         ta = t_cur;
         tb = t_exit;
         if (t_exit >= t1) {
@@ -222,8 +250,9 @@ struct SharedDdaF {
     }
 };
 
-template <int CODEC, int MODE>
-__global__ void __launch_bounds__(kT, kMinBlocks) k_trace_f(const __grid_constant__ RenderArgs A, long long n_units)
+template <int CODEC, int MODE, typename G>
+__global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMixed)
+    k_trace_f(const __grid_constant__ RenderArgs A, long long n_units)
 {
     extern __shared__ float4 s_ent[];
     for (int i = threadIdx.x; i < A.tf.n; i += blockDim.x)
@@ -234,26 +263,31 @@ __global__ void __launch_bounds__(kT, kMinBlocks) k_trace_f(const __grid_constan
     const int tid = threadIdx.x;
     unsigned long long* work = A.counters + 1;
     const TfF tf{float(A.tf.lo), float(1.0 / (A.tf.hi - A.tf.lo)), float(A.tf.scale), A.tf.n, s_ent};
-    const float hi[3] = {float(A.hi[0]), float(A.hi[1]), float(A.hi[2])};
-    const float cell = float(A.cell), icell = float(A.icell);
+    const G hi[3] = {G(A.hi[0]), G(A.hi[1]), G(A.hi[2])};
+    const G cell = G(A.cell), icell = G(A.icell);
+    using Ray = RayG<G>;
 
     // ---- per-lane state: registers for the step loop, shared memory (SoA) for the rest ----
     __shared__ int s_dda_i[7][kT];
-    __shared__ float s_dda_f[8][kT];
-    SharedDdaF dda{&s_dda_i[0][0], &s_dda_f[0][0], tid};
-    __shared__ float s_ray[6][kT];
+    __shared__ G s_dda_f[8][kT];
+    SharedDdaG<G> dda{&s_dda_i[0][0], &s_dda_f[0][0], tid};
+    __shared__ G s_ray[6][kT];
+    __shared__ G s_tev[kT];
     __shared__ int s_acc[14][kT];
     __shared__ double s_sum[3][kT];                    // per-pixel FP64 accumulation
-    __shared__ float s_cold[RATIO ? 9 : 5][kT];        // tp0..2, t_ev, v_ev (+ L0..2, Tr)
+    __shared__ float s_cold[RATIO ? 8 : 5][kT];        // tp0..2, (unused), v_ev (+ L0..2)
+    // ratio transmittance stays FP64: a float product underflows to 0 (ending the flight) long
+    // before the reference's double does, which would change the draws that follow
+    __shared__ double s_tr[RATIO ? kT : 1];
     __shared__ int s_ci[RATIO ? 6 : 5][kT];            // px, py, s, bounces, out_off (+ have)
     volatile float* cold = &s_cold[0][tid];
     volatile int* ci = &s_ci[0][tid];
     volatile double* sum = &s_sum[0][tid];
     auto tp = [&](int k) -> volatile float& { return cold[k * kT]; };
-    volatile float& t_ev = cold[3 * kT];
+    volatile G& t_ev = reinterpret_cast<volatile G*>(s_tev)[tid];
     volatile float& v_ev = cold[4 * kT];
     auto Lr = [&](int k) -> volatile float& { return cold[(5 + k) * kT]; }; // ratio only
-    volatile float& Tr = cold[(RATIO ? 8 : 0) * kT];                          // ratio only
+    volatile double& Tr = reinterpret_cast<volatile double*>(s_tr)[RATIO ? tid : 0]; // ratio only
     volatile int &px = ci[0], &py = ci[kT], &s = ci[2 * kT], &bounces = ci[3 * kT], &out_off = ci[4 * kT];
     volatile int& have = ci[(RATIO ? 5 : 0) * kT]; // ratio only
 
@@ -273,24 +307,29 @@ __global__ void __launch_bounds__(kT, kMinBlocks) k_trace_f(const __grid_constan
     };
     acc_io(true);
     auto ray_load = [&]() {
-        RayF r;
+        Ray r;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            r.o[k] = reinterpret_cast<volatile float*>(s_ray[k])[tid];
-            r.d[k] = reinterpret_cast<volatile float*>(s_ray[3 + k])[tid];
+            r.o[k] = reinterpret_cast<volatile G*>(s_ray[k])[tid];
+            r.d[k] = reinterpret_cast<volatile G*>(s_ray[3 + k])[tid];
         }
         return r;
     };
-    auto ray_store = [&](const RayF& r) {
+    auto ray_store = [&](const Ray& r) {
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            reinterpret_cast<volatile float*>(s_ray[k])[tid] = r.o[k];
-            reinterpret_cast<volatile float*>(s_ray[3 + k])[tid] = r.d[k];
+            reinterpret_cast<volatile G*>(s_ray[k])[tid] = r.o[k];
+            reinterpret_cast<volatile G*>(s_ray[3 + k])[tid] = r.d[k];
         }
     };
 
     RngF rng{0};
-    float t = 0.0f, tb = 0.0f, inv = 0.0f, inv_ahead = 0.0f;
+    constexpr bool MIXED = sizeof(G) == 8;
+    constexpr bool ACC64 = MIXED && SVDB_MIX_ACCEPT64; // accept test in FP64 as the reference
+    using I = typename std::conditional<ACC64, double, float>::type;
+    const I* inv_tab = reinterpret_cast<const I*>(ACC64 ? (const void*)A.inv_maj : (const void*)A.inv_maj_f);
+    G t = G(0), tb = G(0);
+    I inv = I(0), inv_ahead = I(0);
     uint32_t samples = 0;
     int state = kNeedPixel;
     bool done = false;
@@ -306,7 +345,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks) k_trace_f(const __grid_constan
     };
     auto finish_ratio = [&]() { finish_path(Lr(0), Lr(1), Lr(2)); };
     // scattering vertex (render.hpp:173-185)
-    auto bounce = [&](float te, float ve) {
+    auto bounce = [&](G te, float ve) {
         bounces = bounces + 1;
         if (bounces > A.max_bounces) {
             if constexpr (RATIO)
@@ -319,18 +358,30 @@ __global__ void __launch_bounds__(kT, kMinBlocks) k_trace_f(const __grid_constan
         tf.rgb(ve, alb);
         float tpv[3] = {tp(0) * alb[0], tp(1) * alb[1], tp(2) * alb[2]};
         {
-            RayF ray = ray_load();
+            Ray ray = ray_load();
             ray.o[0] += ray.d[0] * te;
             ray.o[1] += ray.d[1] * te;
             ray.o[2] += ray.d[2] * te;
-            const float u0 = rng.uniform(), u1 = rng.uniform();
-            const float z = 1.0f - 2.0f * u0;
-            const float r = sqrtf(fmaxf(0.0f, 1.0f - z * z));
-            float sp, cp;
-            sincospif(2.0f * u1, &sp, &cp);
-            ray.d[0] = r * cp;
-            ray.d[1] = r * sp;
-            ray.d[2] = z;
+            if constexpr (MIXED) { // sample_isotropic (render.hpp:128-134) in FP64: a float
+                // direction would move every later point of the path by ~1e-7 of its length
+                const double u0 = rng.uniform53(), u1 = rng.uniform53();
+                const double z = 1.0 - 2.0 * u0;
+                const double r = sqrt(fmax(0.0, 1.0 - z * z));
+                double sp, cp;
+                sincos(2.0 * 3.14159265358979323846 * u1, &sp, &cp);
+                ray.d[0] = G(r * cp);
+                ray.d[1] = G(r * sp);
+                ray.d[2] = G(z);
+            } else {
+                const float u0 = rng.uniform(), u1 = rng.uniform();
+                const float z = 1.0f - 2.0f * u0;
+                const float r = sqrtf(fmaxf(0.0f, 1.0f - z * z));
+                float sp, cp;
+                sincospif(2.0f * u1, &sp, &cp);
+                ray.d[0] = G(r * cp);
+                ray.d[1] = G(r * sp);
+                ray.d[2] = G(z);
+            }
             ray_store(ray);
         }
         if (bounces >= A.rr_start) {
@@ -354,7 +405,7 @@ __global__ void __launch_bounds__(kT, kMinBlocks) k_trace_f(const __grid_constan
     };
     auto end_segment = [&]() {
         if constexpr (RATIO) {
-            const float tr = Tr;
+            const float tr = float(Tr);
             Lr(0) = Lr(0) + tp(0) * tr * A.ambient[0];
             Lr(1) = Lr(1) + tp(1) * tr * A.ambient[1];
             Lr(2) = Lr(2) + tp(2) * tr * A.ambient[2];
@@ -385,8 +436,15 @@ __global__ void __launch_bounds__(kT, kMinBlocks) k_trace_f(const __grid_constan
                 const Rng r0 = Rng::for_pixel_sample(A.seed_mixed, px, py, s);
                 rng.state = r0.state;
             }
-            const float jx = rng.uniform(), jy = rng.uniform();
-            ray_store(camera_ray_f(A.cam, float(px) + jx, float(py) + jy));
+            G jx, jy;
+            if constexpr (MIXED) {
+                jx = rng.uniform53();
+                jy = rng.uniform53();
+            } else {
+                jx = rng.uniform();
+                jy = rng.uniform();
+            }
+            ray_store(camera_ray_g<G>(A.cam, G(px) + jx, G(py) + jy));
             tp(0) = tp(1) = tp(2) = 1.0f;
             bounces = 0;
             if constexpr (RATIO)
@@ -395,54 +453,64 @@ __global__ void __launch_bounds__(kT, kMinBlocks) k_trace_f(const __grid_constan
         }
     segment:
         if constexpr (RATIO) {
-            Tr = 1.0f;
+            Tr = 1.0;
             have = 0;
         }
         if (!dda.init(A.cells, hi, ray_load(), cell, icell)) {
             end_segment();
             return;
         }
-        inv_ahead = __ldg(A.inv_maj_f + dda.index(A.cells));
+        inv_ahead = __ldg(inv_tab + dda.index(A.cells));
         state = kNeedCell;
     };
     // kNeedCell -> next macrocell (empty cells draw nothing); kInCell -> one tentative step
     auto do_advance = [&]() {
         const float lg = __log2f(1.0f - rng.peek()); // step draw, consumed only where it is used
         if (state == kNeedCell) {
-            float ta, tbb;
-            if ((RATIO && !(Tr > 0.0f)) || !dda.next(A.cells, ta, tbb)) {
+            G ta, tbb;
+            if ((RATIO && !(Tr > 0.0)) || !dda.next(A.cells, ta, tbb)) {
                 end_segment();
                 return;
             }
             inv = inv_ahead;
             if (!dda.done())
-                inv_ahead = __ldg(A.inv_maj_f + dda.index(A.cells));
-            if (!(inv > 0.0f))
+                inv_ahead = __ldg(inv_tab + dda.index(A.cells));
+            if (!(inv > I(0)))
                 return;
             t = ta;
             tb = tbb;
         }
         rng.skip();
-        t -= lg * 0.693147182f * inv;
+        t -= G(lg * 0.693147182f) * G(inv);
         state = t >= tb ? kNeedCell : kPoint;
     };
     auto accept = [&](float v) {
+        if constexpr (ACC64 && !RATIO) { // render.hpp:119-122 in FP64 with the 53-bit draw
+            if (rng.uniform53() < tf_extinction(A.tf, s_ent, double(v)) * inv) {
+                t_ev = t;
+                v_ev = v;
+                state = kScatter;
+            } else {
+                state = kInCell;
+            }
+            return;
+        }
         const float st = tf.extinction(v);
         if constexpr (RATIO) {
-            const float r = st * inv;
+            const float r = float(st * inv);
             if (!have && rng.uniform() < r) {
                 have = 1;
                 t_ev = t;
                 v_ev = v;
             }
-            const float tr = Tr * (1.0f - r);
+            const double tr = Tr * (1.0 - double(r));
             Tr = tr;
             if (!(tr > 0.0f))
                 end_segment();
             else
                 state = kInCell;
         } else {
-            if (rng.uniform() < st * inv) {
+            if (rng.uniform() < float(st * inv)) {
                 t_ev = t;
                 v_ev = v;
                 state = kScatter;
@@ -453,9 +521,14 @@ __global__ void __launch_bounds__(kT, kMinBlocks) k_trace_f(const __grid_constan
     };
     auto do_sample = [&]() {
         acc_io(false);
-        const RayF r = ray_load();
+        const Ray r = ray_load();
         ++samples;
-        const float v = sample_f<CODEC>(acc, r.o[0] + r.d[0] * t, r.o[1] + r.d[1] * t, r.o[2] + r.d[2] * t);
+        float v;
+        if constexpr (MIXED && SVDB_MIX_SAMPLE64) // the reference's FP64 trilinear (sample.hpp:46-72)
+            v = sample_trilinear<CODEC>(acc, double(r.o[0] + r.d[0] * t), double(r.o[1] + r.d[1] * t),
+                                        double(r.o[2] + r.d[2] * t));
+        else
+            v = sample_f<CODEC, G>(acc, r.o[0] + r.d[0] * t, r.o[1] + r.d[1] * t, r.o[2] + r.d[2] * t);
         acc_io(true);
         accept(v);
     };
@@ -527,33 +600,43 @@ __global__ void __launch_bounds__(kT, kMinBlocks) k_trace_f(const __grid_constan
         atomicAdd(A.counters, s64);
 }
 
-template <int CODEC, int MODE>
+template <int CODEC, int MODE, typename G>
 int launch(const RenderArgs& A, long long n_units, size_t smem, cudaStream_t s)
 {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace_f<CODEC, MODE>, kT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace_f<CODEC, MODE, G>, kT, smem);
     const long long blocks = std::min<long long>((long long)std::max(per_sm, 1) * sms, (n_units * 32 + kT - 1) / kT);
-    k_trace_f<CODEC, MODE><<<unsigned(blocks), kT, smem, s>>>(A, n_units);
+    k_trace_f<CODEC, MODE, G><<<unsigned(blocks), kT, smem, s>>>(A, n_units);
     return 0;
+}
+
+template <int CODEC, typename G>
+int launch_mode(const RenderArgs& A, int mode, long long n_units, size_t smem, cudaStream_t s)
+{
+    return mode == SVDBGPU_MODE_RATIO ? launch<CODEC, SVDBGPU_MODE_RATIO, G>(A, n_units, smem, s)
+                                      : launch<CODEC, SVDBGPU_MODE_PATHTRACE, G>(A, n_units, smem, s);
+}
+
+template <typename G>
+int launch_codec(const RenderArgs& A, int codec, int mode, long long n_units, size_t smem, cudaStream_t s)
+{
+    switch (codec) {
+    case kCodecF32: return launch_mode<kCodecF32, G>(A, mode, n_units, smem, s);
+    case kCodecUnorm8: return launch_mode<kCodecUnorm8, G>(A, mode, n_units, smem, s);
+    case kCodecAffine8: return launch_mode<kCodecAffine8, G>(A, mode, n_units, smem, s);
+    default: return launch_mode<kCodecAffine4, G>(A, mode, n_units, smem, s);
+    }
 }
 
 } // namespace
 
-int launch_trace_fast(const RenderArgs& A, int codec, int mode, long long n_units, size_t smem, cudaStream_t s)
+int launch_trace_fast(const RenderArgs& A, int codec, int mode, int precision, long long n_units, size_t smem,
+                      cudaStream_t s)
 {
-    const bool ratio = mode == SVDBGPU_MODE_RATIO;
-    switch (codec) {
-    case kCodecF32: return ratio ? launch<kCodecF32, SVDBGPU_MODE_RATIO>(A, n_units, smem, s)
-                                 : launch<kCodecF32, SVDBGPU_MODE_PATHTRACE>(A, n_units, smem, s);
-    case kCodecUnorm8: return ratio ? launch<kCodecUnorm8, SVDBGPU_MODE_RATIO>(A, n_units, smem, s)
-                                    : launch<kCodecUnorm8, SVDBGPU_MODE_PATHTRACE>(A, n_units, smem, s);
-    case kCodecAffine8: return ratio ? launch<kCodecAffine8, SVDBGPU_MODE_RATIO>(A, n_units, smem, s)
-                                     : launch<kCodecAffine8, SVDBGPU_MODE_PATHTRACE>(A, n_units, smem, s);
-    default: return ratio ? launch<kCodecAffine4, SVDBGPU_MODE_RATIO>(A, n_units, smem, s)
-                          : launch<kCodecAffine4, SVDBGPU_MODE_PATHTRACE>(A, n_units, smem, s);
-    }
+    return precision == SVDBGPU_PRECISION_FP32 ? launch_codec<float>(A, codec, mode, n_units, smem, s)
+                                               : launch_codec<double>(A, codec, mode, n_units, smem, s);
 }
 
 } // namespace svdbgpu
