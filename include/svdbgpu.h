@@ -62,7 +62,7 @@ enum {
    two keep the reference's algorithm and per-pixel draw order: FP32 runs everything in single
    precision; MIXED keeps ray origins/directions, distances and the DDA in FP64 and runs the step
    log, uniforms, transfer function, trilinear weights and throughput in FP32. Both match the
-   reference images within a tolerance instead of bit for bit (DESIGN.md §3.4). */
+   reference images within a tolerance instead of bit for bit (DESIGN.md §3.3). */
 enum { SVDBGPU_PRECISION_FP64 = 0, SVDBGPU_PRECISION_FP32 = 1, SVDBGPU_PRECISION_MIXED = 2 };
 
 /* Kernel variants for A/B measurement; both produce bit-identical images. */

@@ -214,7 +214,7 @@ class RenderSettings:
     majorant_cell: int = 0
     # tracking arithmetic (pathtrace / ratio): 0 = FP64 reference-exact (bit parity); 2 = mixed
     # (FP64 ray / DDA / distances, FP32 step log, sampler, TF, throughput) and 1 = all FP32, both
-    # matching the FP64 image within a tolerance at matched streams (DESIGN.md §3.4)
+    # matching the FP64 image within a tolerance at matched streams (DESIGN.md §3.3)
     precision: int = 0
 
     def _c(self, tile_rank: int = 0, tile_nranks: int = 1) -> N.Settings:
