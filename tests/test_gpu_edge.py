@@ -1,0 +1,110 @@
+"""Edge cases of the render path on the B200 against the unmodified reference (oracle/_ref) and the
+C restatement, the way the reference's own tests probe them (test_render.cpp, test_dda.cpp):
+non-cubic grids with tiles and a non-zero background, cameras inside the volume, images whose size
+is not a multiple of the 16x16 tile, 1x1 frames, zero bounces / immediate Russian roulette, and
+rays that never meet the grid.
+"""
+import numpy as np
+import pytest
+
+import paper_2504_04564_b200 as P
+from helpers import SplitMix, image_parity
+
+pytestmark = pytest.mark.gpu
+
+RMSE_TOL = 1e-3
+
+
+def _tile_grid(ref, dims=(70, 45, 33), background=0.3, seed=11):
+    """Voxels, leaf-sized tiles (kind 1) over a non-cubic grid with a non-zero background."""
+    r = SplitMix(seed)
+    ops = []
+    for _ in range(3000):
+        c = (int(r.uniform() * dims[0]), int(r.uniform() * dims[1]), int(r.uniform() * dims[2]))
+        ops.append((0, c, float(np.float32(r.uniform()))))
+    for _ in range(40):
+        o = (8 * int(r.uniform() * (dims[0] // 8)), 8 * int(r.uniform() * (dims[1] // 8)),
+             8 * int(r.uniform() * (dims[2] // 8)))
+        ops.append((1, o, float(np.float32(r.uniform()))))
+    return ref.build_ops(dims, background, ops)
+
+
+TF = P.TransferFunction(0.0, 1.0, [[0.9, 0.8, 0.7, 0.0], [0.6, 0.9, 0.8, 0.5], [0.9, 0.9, 0.9, 1.0]], 0.08)
+
+
+def _check(img, want, min_same=0.98):
+    same, rmse = image_parity(img, want)
+    print(f"identical {same:.4f} rel RMSE {rmse:.2e}")
+    assert rmse <= RMSE_TOL and same >= min_same
+
+
+@pytest.mark.parametrize("codec", [P.Codec.f32, P.Codec.affine8])
+@pytest.mark.parametrize("mode", [P.RenderMode.pathtrace, P.RenderMode.iso, P.RenderMode.ratio])
+def test_tiles_background_noncubic(gpu, ref, orc, codec, mode):
+    svdb = _tile_grid(ref)
+    g = P.DeviceGrid(svdb, codec)
+    src = svdb if codec == P.Codec.f32 else orc.quantize(svdb, int(codec))[0]
+    cam = P.Camera(position=(140.0, 90.0, -60.0), look_at=(35.0, 22.0, 16.0), fov_y_deg=40.0, width=53, height=37)
+    st = P.RenderSettings(spp=8, seed=5, mode=mode, iso_value=0.45, background_color=(0.2, 0.1, 0.05))
+    img = P.render(g, TF, cam, st).pixels
+    if mode == P.RenderMode.ratio:
+        want, _, _ = orc.open(src).render(TF, cam, st)
+    else:
+        want = ref.open(src).render(TF, cam, st)
+    _check(img, want)
+
+
+@pytest.mark.parametrize("mode", [P.RenderMode.pathtrace, P.RenderMode.ratio, P.RenderMode.ea])
+def test_camera_inside_volume(gpu, ref, orc, mode):
+    svdb = _tile_grid(ref, dims=(64, 64, 64), background=0.05, seed=3)
+    g = P.DeviceGrid(svdb, P.Codec.f32)
+    cam = P.Camera(position=(30.2, 33.7, 29.9), look_at=(50.0, 10.0, 60.0), fov_y_deg=70.0, width=40, height=24)
+    st = P.RenderSettings(spp=6, seed=9, mode=mode)
+    img = P.render(g, TF, cam, st).pixels
+    if mode == P.RenderMode.pathtrace:
+        want = ref.open(svdb).render(TF, cam, st)
+    else:
+        want, _, _ = orc.open(svdb).render(TF, cam, st)
+    _check(img, want)
+
+
+@pytest.mark.parametrize("wh", [(1, 1), (17, 33), (31, 16), (16, 1)])
+def test_odd_image_sizes(gpu, ref, wh):
+    svdb = _tile_grid(ref, dims=(40, 40, 40), seed=21)
+    g = P.DeviceGrid(svdb, P.Codec.f32)
+    cam = P.Camera(position=(19.5, 19.5, -70.0), look_at=(19.5, 19.5, 19.5), width=wh[0], height=wh[1])
+    st = P.RenderSettings(spp=16, seed=2)
+    img = P.render(g, TF, cam, st)
+    assert img.pixels.shape == (wh[1], wh[0], 3)
+    assert img.stats["paths"] == wh[0] * wh[1] * 16
+    _check(img.pixels, ref.open(svdb).render(TF, cam, st), min_same=0.95)
+
+
+@pytest.mark.parametrize("bounces,rr", [(0, 3), (1, 0), (64, 0), (2, 1)])
+def test_bounce_limits_and_roulette(gpu, ref, bounces, rr):
+    # trace_path's cutoff (++bounces > max_bounces -> 0) and RR from rr_start (render.hpp:171-185)
+    svdb = _tile_grid(ref, dims=(48, 48, 48), background=0.4, seed=8)
+    g = P.DeviceGrid(svdb, P.Codec.f32)
+    cam = P.Camera(position=(23.5, 60.0, -50.0), look_at=(23.5, 23.5, 23.5), width=32, height=32)
+    st = P.RenderSettings(spp=8, seed=13, max_bounces=bounces, rr_start_bounce=rr)
+    _check(P.render(g, TF, cam, st).pixels, ref.open(svdb).render(TF, cam, st))
+
+
+def test_rays_missing_the_grid_see_ambient(gpu, ref):
+    svdb = _tile_grid(ref, dims=(32, 32, 32), seed=4)
+    g = P.DeviceGrid(svdb, P.Codec.f32)
+    cam = P.Camera(position=(500.0, 500.0, 500.0), look_at=(900.0, 800.0, 700.0), width=16, height=16)
+    st = P.RenderSettings(spp=4, ambient_radiance=(0.25, 0.5, 0.75))
+    img = P.render(g, TF, cam, st).pixels
+    assert np.all(img == np.array([0.25, 0.5, 0.75], np.float32))
+    assert np.array_equal(img, ref.open(svdb).render(TF, cam, st))
+
+
+def test_far_positions_sample_background(gpu, ref):
+    # sample.hpp lattice_coord clamp at +-1e9 (test_sample.cpp:28-73: background at +-1e30)
+    svdb = _tile_grid(ref, dims=(32, 32, 32), background=0.3, seed=4)
+    g = P.DeviceGrid(svdb, P.Codec.f32)
+    xyz = np.array([[1e30, 0, 0], [-1e30, 5, 5], [3e9, -3e9, 1e12], [np.float64(-0.0), 0.0, 0.0]], np.float64)
+    got = g.sample(xyz)
+    want = ref.open(svdb).sample(xyz)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
