@@ -360,7 +360,8 @@ __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : 
 
 __device__ __forceinline__ double tf_normalized(const DevTF& tf, double v)
 {
-    return dclamp((v - tf.lo) / (tf.hi - tf.lo), 0.0, 1.0);
+    const double d = v - tf.lo;
+    return dclamp(tf.inv_range != 0.0 ? d * tf.inv_range : d / (tf.hi - tf.lo), 0.0, 1.0);
 }
 
 __device__ __forceinline__ void tf_lookup(const DevTF& tf, const float4* ent, double v, double out[4])

@@ -391,7 +391,13 @@ int GridImpl::upload_tf(const svdbgpu_tf* tf, cudaStream_t s, DevTF* out)
         tf_cap = tf->n_entries;
     }
     SVDB_CUDA(cudaMemcpyAsync(d_tf, tf->rgba, sizeof(float4) * size_t(tf->n_entries), cudaMemcpyHostToDevice, s));
-    *out = DevTF{tf->domain_lo, tf->domain_hi, tf->density_scale, tf->n_entries};
+    *out = DevTF{tf->domain_lo, tf->domain_hi, tf->density_scale, tf->n_entries, 0.0};
+    {
+        const double range = tf->domain_hi - tf->domain_lo;
+        int e = 0;
+        if (std::isfinite(range) && range > 0.0 && std::frexp(range, &e) == 0.5 && e > -1000 && e < 1000)
+            out->inv_range = std::ldexp(1.0, 1 - e); // exact reciprocal of the power of two
+    }
     return 0;
 }
 

@@ -30,6 +30,9 @@ struct DevGrid {
 struct DevTF {
     double lo, hi, scale;
     int n;
+    // 1 / (hi - lo) when hi - lo is a power of two (then (v - lo) * inv_range == (v - lo) / (hi - lo)
+    // exactly and the per-lookup FP64 division is skipped), else 0
+    double inv_range;
 };
 
 constexpr int kCodecF32 = 0, kCodecUnorm8 = 1, kCodecAffine8 = 2, kCodecAffine4 = 3;
