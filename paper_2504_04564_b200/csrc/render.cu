@@ -464,6 +464,7 @@ struct SharedDda {
     __device__ __forceinline__ int cy() { return ci(1); }
     __device__ __forceinline__ int cz() { return ci(2); }
     __device__ __forceinline__ bool done() { return ci(6) != 0; }
+    __device__ __forceinline__ int index(const int cells[3]) { return ci(0) + cells[0] * (ci(1) + cells[1] * ci(2)); }
 
     // clip_ray_box + dda_traverse setup (dda.hpp:25-86). Rolled per-axis loops keep one copy of
     // each FP64 division in the instruction stream (this runs once per flight segment); the
@@ -552,6 +553,86 @@ struct SharedDda {
     }
 };
 
+// The moving part of a SharedDda (cell, t_next, t_cur, t1, done) held in registers across one
+// advance phase; step and t_delta are read from shared memory only for the axis that steps.
+// next() is SharedDda::next's arithmetic exactly.
+template <int T>
+struct DdaRegs {
+    SharedDda<T>* s;
+    int c[3];
+    double n[3], t_cur, t1;
+    bool dn;
+    __device__ __forceinline__ void load(SharedDda<T>& d)
+    {
+        s = &d;
+        c[0] = d.ci(0);
+        c[1] = d.ci(1);
+        c[2] = d.ci(2);
+        n[0] = d.cd(0);
+        n[1] = d.cd(1);
+        n[2] = d.cd(2);
+        t_cur = d.cd(6);
+        t1 = d.cd(7);
+        dn = d.ci(6) != 0;
+    }
+    __device__ __forceinline__ void store()
+    {
+        s->ci(0) = c[0];
+        s->ci(1) = c[1];
+        s->ci(2) = c[2];
+        s->cd(0) = n[0];
+        s->cd(1) = n[1];
+        s->cd(2) = n[2];
+        s->cd(6) = t_cur;
+        s->ci(6) = dn ? 1 : 0;
+    }
+    __device__ __forceinline__ bool done() const { return dn; }
+    __device__ __forceinline__ int index(const int cells[3]) const { return c[0] + cells[0] * (c[1] + cells[1] * c[2]); }
+    __device__ __forceinline__ bool next(const int cells[3], int cell[3], double& ta, double& tb)
+    {
+        if (dn)
+            return false;
+        const bool ax1 = n[1] < n[0];
+        const double tm = ax1 ? n[1] : n[0];
+        const bool ax2 = n[2] < tm;
+        const int axis = ax2 ? 2 : (ax1 ? 1 : 0);
+        double t_exit = dmin(ax2 ? n[2] : tm, t1);
+        t_exit = dmax(t_exit, t_cur);
+        cell[0] = c[0];
+        cell[1] = c[1];
+        cell[2] = c[2];
+        ta = t_cur;
+        tb = t_exit;
+        if (t_exit >= t1) {
+            dn = true;
+            return true;
+        }
+        t_cur = t_exit;
+        const int cn = (axis == 0 ? c[0] : (axis == 1 ? c[1] : c[2])) + s->ci(3 + axis);
+        if (axis == 0)
+            c[0] = cn;
+        else if (axis == 1)
+            c[1] = cn;
+        else
+            c[2] = cn;
+        if (cn < 0 || cn >= cells[axis]) {
+            dn = true;
+        } else {
+            const double nn = (axis == 0 ? n[0] : (axis == 1 ? n[1] : n[2])) + s->cd(3 + axis);
+            if (axis == 0)
+                n[0] = nn;
+            else if (axis == 1)
+                n[1] = nn;
+            else
+                n[2] = nn;
+        }
+        return true;
+    }
+};
+
+#ifndef SVDB_DDA_REGS
+#define SVDB_DDA_REGS 0
+#endif
 #ifndef SVDB_TRACE_THREADS
 #define SVDB_TRACE_THREADS 64 // 2 warps per CTA, <= 80 registers: 24 resident warps per SM
 #endif
@@ -560,6 +641,9 @@ struct SharedDda {
 #endif
 #ifndef SVDB_SCHED
 #define SVDB_SCHED 1 // 0: advance-to-point then gather; 1: per-iteration phase selection
+#endif
+#ifndef SVDB_W_SAMPLE_DEN
+#define SVDB_W_SAMPLE_DEN 1
 #endif
 #ifndef SVDB_W_SAMPLE
 #define SVDB_W_SAMPLE 1
@@ -842,7 +926,7 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
     };
     // kNeedCell -> next macrocell (empty cells draw nothing, render.hpp:145-146);
     // kInCell -> one tentative step t -= ln(1-u)/sigma_maj (render.hpp:116-118)
-    auto do_advance = [&]() {
+    auto do_advance = [&](auto& D) {
 #if SVDB_SPEC_LOG
         // the step draw's log does not depend on the DDA: compute it from the next uniform before
         // the cell lookup (independent FP64 chains interleave); the draw is consumed only if the
@@ -852,7 +936,7 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         if (state == kNeedCell) {
             int c[3];
             double ta, tbb;
-            if ((RATIO && !(Tr > 0.0)) || !dda.next(A.cells, c, ta, tbb)) {
+            if ((RATIO && !(Tr > 0.0)) || !D.next(A.cells, c, ta, tbb)) {
                 end_segment();
                 return;
             }
@@ -864,8 +948,8 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             // the majorant of this cell was loaded one visit ahead; issue the next cell's now
             // (dda.c already holds the following cell) so the load overlaps a whole iteration
             inv = inv_ahead;
-            if (!dda_done())
-                inv_ahead = __ldg(A.inv_maj + dda_cur_index());
+            if (!D.done())
+                inv_ahead = __ldg(A.inv_maj + D.index(A.cells));
 #else
             inv = __ldg(A.inv_maj + tr.cell_index(c));
 #endif
@@ -994,7 +1078,8 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter));
             // start lanes may wait to batch up, but a non-empty phase is always chosen
             const int nTw = nT > 0 ? max(1, nT * SVDB_W_START_NUM / SVDB_W_START_DEN) : 0;
-            const int phase = (nS * SVDB_W_SAMPLE >= nA && nS * SVDB_W_SAMPLE >= nTw) ? 2 : (nA >= nTw ? 1 : 0);
+            const int nSw = nS * SVDB_W_SAMPLE / SVDB_W_SAMPLE_DEN;
+            const int phase = (nS > 0 && nSw >= nA && nSw >= nTw) || (nA == 0 && nTw == 0) ? 2 : (nA >= nTw ? 1 : 0);
 #ifdef SVDB_PHASE_STATS
             if (lane == __ffs(live) - 1) { // per phase: invocations and participating lanes
                 const int n = phase == 0 ? nT : (phase == 1 ? nA : nS);
@@ -1018,18 +1103,30 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
                     if (n == 0 || k >= SVDB_ADV_ITERS || n * SVDB_ADV_FRAC < nA)
                         break;
                     if (adv)
-                        do_advance();
+                        do_advance(dda);
+                }
+#else
+#if SVDB_DDA_REGS
+                if (state == kNeedCell || state == kInCell) {
+                    // the DDA's moving state lives in registers for the whole advance phase
+                    DdaRegs<SVDB_TRACE_THREADS> R;
+                    R.load(dda);
+#pragma unroll 1
+                    for (int k = 0; k < SVDB_ADV_ITERS && (state == kNeedCell || state == kInCell); ++k)
+                        do_advance(R);
+                    R.store();
                 }
 #else
 #pragma unroll 1
                 for (int k = 0; k < SVDB_ADV_ITERS && (state == kNeedCell || state == kInCell); ++k)
-                    do_advance();
+                    do_advance(dda);
+#endif
 #endif
             } else if (state == kPoint) {
                 do_sample();
 #pragma unroll 1
                 for (int k = 0; k < SVDB_GATHER_ADV && (state == kNeedCell || state == kInCell); ++k)
-                    do_advance(); // rejected collisions draw their next step at once
+                    do_advance(dda); // rejected collisions draw their next step at once
             }
 #ifdef SVDB_PHASE_STATS
             __syncwarp(live);
@@ -1044,7 +1141,7 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             if (state == kNeedPath || state == kNeedSegment || state == kScatter)
                 do_start();
             else
-                do_advance();
+                do_advance(dda);
         }
         if (state == kPoint)
             do_sample();
