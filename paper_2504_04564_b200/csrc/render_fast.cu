@@ -35,9 +35,15 @@ namespace svdbgpu {
 namespace {
 
 constexpr int kT = 64;          // threads per CTA
-constexpr int kMinBlocks = 16;  // 32 warps per SM (pure FP32)
-constexpr int kMinBlocksMixed = 12; // FP64 geometry: 264 B of shared state per lane
-constexpr int kAdvIters = 3;    // advance steps per advance-phase invocation
+#ifndef SVDB_F_MIN_BLOCKS_MIXED
+#define SVDB_F_MIN_BLOCKS_MIXED 12
+#endif
+#ifndef SVDB_F_ADV_ITERS
+#define SVDB_F_ADV_ITERS 3
+#endif
+constexpr int kMinBlocks = 16;                           // 32 warps per SM (pure FP32)
+constexpr int kMinBlocksMixed = SVDB_F_MIN_BLOCKS_MIXED; // FP64 geometry: 264 B of shared state per lane
+constexpr int kAdvIters = SVDB_F_ADV_ITERS;              // advance steps per advance-phase invocation
 constexpr unsigned kFull = 0xffffffffu;
 
 enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4, kPoint = 5, kScatter = 6 };
