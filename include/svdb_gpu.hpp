@@ -277,5 +277,17 @@ inline std::vector<uint8_t> compress(const float* data, const std::array<int32_t
     return v;
 }
 
+/// SVDB v1 -> quantised SVDB v2 (N-bit leaf codes + per-leaf lo/scale, encoded by the device codec);
+/// Grid(v2) equals Grid(v1, codec).
+inline std::vector<uint8_t> quantise(const std::vector<uint8_t>& svdb, Codec codec = Codec::auto8, int device = 0)
+{
+    uint8_t* out = nullptr;
+    size_t n = 0;
+    check(svdbgpu_quantise(svdb.data(), svdb.size(), int32_t(codec), device, &out, &n));
+    std::vector<uint8_t> v(out, out + n);
+    svdbgpu_free(out);
+    return v;
+}
+
 } // namespace gpu
 } // namespace svdb

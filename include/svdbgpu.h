@@ -11,6 +11,7 @@
  *   svdbgpu_macrocells      <- build_macrocells()+update_majorants() macrocell.hpp:74-116
  *   svdbgpu_render          <- render(grid,tf,cam,rs)    render.hpp:319-325 (render_field 276-315)
  *   svdbgpu_compress        <- compress(volume,params)   compress.hpp:221-283 (host encoder)
+ *   svdbgpu_quantise        <- serialize_frozen()        io.hpp:121-175 (+ quantised leaf section, new)
  *
  * Conventions: plain pointers and sizes only; every function returns 0 on success, svdb::Errc+1
  * (errors.hpp:11-23: 1 IoError .. 11 DimsMismatch) for the reference's own error classes, or one
@@ -183,6 +184,15 @@ int svdbgpu_unpack_tiles_device(const float* d_packed, int32_t nranks, int64_t m
 int svdbgpu_compress(const float* data, const int32_t dims[3], int32_t voxel_type, double quality,
                      int32_t metric /*0 closest,1 farthest,2 median*/, int32_t threads,
                      uint8_t** svdb_out, size_t* n_out, svdbgpu_compress_report* report);
+
+/* ---- quantised container: SVDB v1 -> "SVDB v2" with N-bit leaves ----
+ * Same header / root / upper / lower sections as v1 (io.hpp:22-43) with version 2 and the codec in
+ * the header's padding word (offset 68); each leaf record is {origin 3 x i32, pad, active mask 512
+ * bits, lo f32, scale f32, codes (512 B UNORM8/AFFINE8, 256 B AFFINE4)} — 600 / 344 B instead of
+ * 2128 B. The codes are the device codec's (a v2 file loads to exactly the grid svdbgpu_grid_create
+ * builds from the v1 file with that codec). svdbgpu_grid_create accepts v2 with codec AUTO8 or the
+ * stored codec. *out is freed with svdbgpu_free. */
+int svdbgpu_quantise(const uint8_t* svdb, size_t n, int32_t codec, int32_t device, uint8_t** out, size_t* n_out);
 
 /* ---- synthetic volumes (host, deterministic; x fastest) ----
  * kind 0 Marschner-Lobb (u8-quantised, values k/255), 1 fBm smoke (u8-quantised),

@@ -75,6 +75,7 @@ SIGNATURES = {
                                    C.c_int32, C.POINTER(P), C.POINTER(C.c_size_t),
                                    C.POINTER(CompressReport)]),
     "svdbgpu_synth": (C.c_int, [C.c_int32, C.POINTER(C.c_int32), C.c_uint64, C.c_int32, P]),
+    "svdbgpu_quantise": (C.c_int, [P, C.c_size_t, C.c_int32, C.c_int32, C.POINTER(P), C.POINTER(C.c_size_t)]),
 }
 
 _lib = None

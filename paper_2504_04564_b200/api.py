@@ -134,6 +134,21 @@ def compress(volume: np.ndarray, params: CompressionParams = CompressionParams()
                                    rep.achieved_ratio)
 
 
+def quantise(svdb: bytes, codec: "Codec" = None, device: int = 0) -> bytes:
+    """SVDB v1 -> quantised SVDB v2 (leaves as N-bit codes + per-leaf lo/scale, encoded on the GPU
+    with the device codec; include/svdbgpu.h ``svdbgpu_quantise``). ``DeviceGrid`` loads the result
+    to exactly the grid it builds from the v1 bytes with that codec."""
+    codec = Codec.auto8 if codec is None else codec
+    buf = np.frombuffer(svdb, dtype=np.uint8) if len(svdb) else np.zeros(1, np.uint8)
+    out = C.c_void_p()
+    n = C.c_size_t()
+    L = N.lib()
+    _check(L.svdbgpu_quantise(buf.ctypes.data, len(svdb), int(codec), device, C.byref(out), C.byref(n)))
+    data = _take_bytes(out, n.value)
+    L.svdbgpu_free(out)
+    return data
+
+
 SYNTH_KINDS = {"marschner_lobb": 0, "fbm_smoke": 1, "turbulence": 2, "sparse": 3}
 
 

@@ -363,6 +363,25 @@ int svdbgpu_compress(const float* data, const int32_t dims[3], int32_t voxel_typ
     });
 }
 
+int svdbgpu_quantise(const uint8_t* svdb, size_t n, int32_t codec, int32_t device, uint8_t** out, size_t* n_out)
+{
+    if (!svdb || !out || !n_out)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "null argument");
+    return guarded([&] {
+        std::vector<uint8_t> bytes;
+        int rc = quantise_svdb(svdb, n, codec, device, bytes);
+        if (rc)
+            return rc;
+        auto* p = static_cast<uint8_t*>(std::malloc(bytes.size() ? bytes.size() : 1));
+        if (!p)
+            return fail_code(SVDBGPU_E_OOM, "host allocation failed");
+        std::memcpy(p, bytes.data(), bytes.size());
+        *out = p;
+        *n_out = bytes.size();
+        return 0;
+    });
+}
+
 int svdbgpu_synth(int32_t kind, const int32_t dims[3], uint64_t seed, int32_t threads, float* out)
 {
     if (!dims || !out || kind < 0 || kind > 3)

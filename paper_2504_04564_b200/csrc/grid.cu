@@ -113,6 +113,26 @@ __global__ void __launch_bounds__(256) k_leaf_encode(const uint8_t* __restrict__
     }
 }
 
+// SVDB v2 (quantised leaves, `svdbgpu_quantise`): the records already hold the codes and the
+// per-leaf (lo, scale); copy them into the strided device layout, 8 B per lane step.
+// Record: origin/pad 16 B | active mask 64 B | lo, scale 8 B | codes main_bytes.
+__global__ void __launch_bounds__(256) k_leaf_load(const uint8_t* __restrict__ staging, uint64_t n_leaf,
+                                                   uint32_t rec, uint32_t main_bytes, uint8_t* __restrict__ codes_base,
+                                                   uint32_t stride, float2* __restrict__ params)
+{
+    const int lane = threadIdx.x & 31;
+    const uint64_t leaf = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (leaf >= n_leaf)
+        return;
+    const uint8_t* r = staging + leaf * rec;
+    const uint2* s2 = reinterpret_cast<const uint2*>(r + 88);
+    uint2* d2 = reinterpret_cast<uint2*>(codes_base + leaf * stride);
+    for (uint32_t i = lane; i < main_bytes / 8; i += 32)
+        d2[i] = __ldg(s2 + i);
+    if (lane == 0)
+        params[leaf] = *reinterpret_cast<const float2*>(r + 80);
+}
+
 // Lower slot table with the child leaf's decode parameters folded in (one 16-B load per miss).
 __global__ void k_expand_lower(const uint2* __restrict__ staged, uint64_t n_slots,
                                const float2* __restrict__ params, uint4* __restrict__ lower)
@@ -475,7 +495,7 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
     if (n < 8)
         return fail(Errc::corrupt_index, "unexpected end of SVDB data");
     uint32_t version = rd_u32(b + 4);
-    if (version != 1)
+    if (version != 1 && version != 2)
         return fail(Errc::version_mismatch, "unsupported SVDB version " + std::to_string(version));
     if (n < kHdr)
         return fail(Errc::corrupt_index, "unexpected end of SVDB data");
@@ -489,7 +509,19 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
     const uint64_t lim = 1ull << 32;
     if (nu > lim || nl > lim || nf > lim || nr > lim)
         return fail(Errc::corrupt_index, "implausible section counts");
-    if (kHdr + kRootRec * nr + kUpperRec * nu + kLowerRec * nl + kLeafRec * nf != n)
+    // v2 (this repo's quantised-leaf container, svdbgpu_quantise): the v1 layout with the codec in
+    // the header's padding word and leaf records {origin/pad, active mask, lo/scale, codes}
+    int stored = -1;
+    uint64_t leaf_rec = kLeafRec;
+    if (version == 2) {
+        stored = int(rd_u32(b + 68));
+        if (stored != kCodecUnorm8 && stored != kCodecAffine8 && stored != kCodecAffine4)
+            return fail(Errc::corrupt_index, "invalid quantised leaf codec");
+        if (codec != SVDBGPU_CODEC_AUTO8 && codec != stored)
+            return fail_code(SVDBGPU_E_UNSUPPORTED, "a quantised SVDB is loaded with its stored codec (or AUTO8)");
+        leaf_rec = 88 + (stored == kCodecAffine4 ? 256 : 512);
+    }
+    if (kHdr + kRootRec * nr + kUpperRec * nu + kLowerRec * nl + leaf_rec * nf != n)
         return fail(Errc::corrupt_index, "section counts do not match data size");
     const uint8_t* root = b + kHdr;
     const uint8_t* up = root + kRootRec * nr;
@@ -573,8 +605,8 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
     }
 
     // ---- leaves: stage records in chunks, encode with the codec, then build the aprons ----
-    int resolved = codec;
-    if (codec == SVDBGPU_CODEC_AUTO8)
+    int resolved = stored >= 0 ? stored : codec;
+    if (resolved == SVDBGPU_CODEC_AUTO8)
         resolved = vt == 0 ? kCodecUnorm8 : kCodecAffine8;
     const uint32_t main_bytes = resolved == kCodecF32 ? 2048u : (resolved == kCodecAffine4 ? 256u : 512u);
     const uint32_t stride = main_bytes + (resolved == kCodecF32 ? 880u : 256u); // + 217-entry apron
@@ -583,7 +615,7 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
     uint8_t* d_stage = nullptr;
     int4* d_lorg = nullptr;
     int* d_bad = nullptr;
-    const uint64_t chunk = std::min<uint64_t>(nf ? nf : 1, 1ull << 18); // 256 Ki leaves = 558 MB staging
+    const uint64_t chunk = std::min<uint64_t>(nf ? nf : 1, 1ull << 18); // 256 Ki leaves <= 558 MB staging
     SVDB_CUDA(cudaMalloc(&d_params, sizeof(float2) * (nf ? nf : 1)));
     SVDB_CUDA(cudaMalloc(&d_bad, sizeof(int)));
     SVDB_CUDA(cudaMalloc(&g->d_codes, size_t(stride) * (nf ? nf : 1)));
@@ -595,7 +627,7 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
         SVDB_CUDA(cudaMemcpyAsync(d_lstage, h_lower.data(), sizeof(uint2) * h_lower.size(), cudaMemcpyHostToDevice, s));
     }
     if (nf)
-        SVDB_CUDA(cudaMalloc(&d_stage, size_t(kLeafRec * chunk)));
+        SVDB_CUDA(cudaMalloc(&d_stage, size_t(leaf_rec * chunk)));
     g->dg.dims[0] = dims[0];
     g->dg.dims[1] = dims[1];
     g->dg.dims[2] = dims[2];
@@ -612,13 +644,17 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
         SVDB_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
         for (uint64_t first = 0; first < nf; first += chunk) {
             uint64_t cnt = std::min(chunk, nf - first);
-            SVDB_CUDA(cudaMemcpyAsync(d_stage, leaf + kLeafRec * first, size_t(kLeafRec * cnt), cudaMemcpyHostToDevice, s));
+            SVDB_CUDA(cudaMemcpyAsync(d_stage, leaf + leaf_rec * first, size_t(leaf_rec * cnt), cudaMemcpyHostToDevice, s));
             unsigned blocks = unsigned((cnt + 7) / 8);
             uint8_t* dst = g->d_codes + size_t(stride) * first;
             float2* par = d_params + first;
+            if (stored >= 0) {
+                k_leaf_load<<<blocks, 256, 0, s>>>(d_stage, cnt, uint32_t(leaf_rec), main_bytes, dst, stride, par);
+            } else {
 #define LAUNCH_ENCODE(C) k_leaf_encode<C><<<blocks, 256, 0, s>>>(d_stage, cnt, dst, stride, par, d_bad)
-            SVDB_CODEC_DISPATCH(resolved, LAUNCH_ENCODE)
+                SVDB_CODEC_DISPATCH(resolved, LAUNCH_ENCODE)
 #undef LAUNCH_ENCODE
+            }
             SVDB_CUDA(cudaGetLastError());
         }
         if (nl) {
@@ -637,7 +673,7 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
         SVDB_CUDA(cudaStreamSynchronize(s));
         if (!bad)
             break;
-        if (codec == SVDBGPU_CODEC_AUTO8 && resolved == kCodecUnorm8) {
+        if (codec == SVDBGPU_CODEC_AUTO8 && resolved == kCodecUnorm8 && stored < 0) {
             resolved = kCodecAffine8; // same layout
             continue;
         }
@@ -714,6 +750,45 @@ int gradient_device(const GridImpl* g, const double* d_xyz, size_t n, double* d_
     SVDB_CODEC_DISPATCH(g->codec, LAUNCH_G)
 #undef LAUNCH_G
     SVDB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+
+// svdbgpu_quantise: SVDB v1 -> v2 with the leaves encoded on the GPU by the device codec (the
+// k_leaf_encode arithmetic). Header, root, upper and lower sections are kept byte for byte (version
+// 2, codec in the padding word); each leaf record keeps its origin and active mask and carries
+// (lo, scale) + codes instead of 512 floats: 600 B (8-bit) / 344 B (4-bit) vs 2128 B.
+int quantise_svdb(const uint8_t* b, size_t n, int codec, int device, std::vector<uint8_t>& out)
+{
+    if (codec != kCodecUnorm8 && codec != kCodecAffine8 && codec != kCodecAffine4 && codec != SVDBGPU_CODEC_AUTO8)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "quantise needs UNORM8, AFFINE8, AFFINE4 or AUTO8");
+    if (n >= 8 && std::memcmp(b, "SVDB", 4) == 0 && rd_u32(b + 4) != 1)
+        return fail(Errc::version_mismatch, "quantise reads SVDB version 1");
+    GridImpl* gp = nullptr;
+    if (int rc = grid_create(b, n, codec, device, &gp))
+        return rc;
+    std::unique_ptr<GridImpl> g(gp);
+    const uint64_t nf = g->n_leaf, nl = g->n_lower, nu = g->n_upper, nr = g->n_root;
+    const uint32_t mb = g->dg.main_bytes;
+    const uint64_t head = kHdr + kRootRec * nr + kUpperRec * nu + kLowerRec * nl;
+    const uint64_t rec = 88 + mb;
+    std::vector<uint8_t> codes(size_t(mb) * (nf ? nf : 1));
+    std::vector<float> params(2 * size_t(nf ? nf : 1));
+    if (nf)
+        if (int rc = grid_leaf_codes(g.get(), 0, nf, codes.data(), params.data()))
+            return rc;
+    out.resize(size_t(head + rec * nf));
+    std::memcpy(out.data(), b, size_t(head));
+    const uint32_t v2 = 2, cv = uint32_t(g->codec);
+    std::memcpy(out.data() + 4, &v2, 4);
+    std::memcpy(out.data() + 68, &cv, 4);
+    const uint8_t* leaf = b + head;
+    for (uint64_t i = 0; i < nf; ++i) {
+        uint8_t* d = out.data() + head + rec * i;
+        std::memcpy(d, leaf + kLeafRec * i, 80); // origin, pad, active mask
+        std::memcpy(d + 80, &params[2 * i], 8);
+        std::memcpy(d + 88, codes.data() + size_t(mb) * i, mb);
+    }
     return 0;
 }
 

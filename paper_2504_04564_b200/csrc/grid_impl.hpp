@@ -68,6 +68,7 @@ struct GridImpl {
 int validate_tf(const svdbgpu_tf* tf);
 int grid_create(const uint8_t* svdb, size_t n, int codec, int device, GridImpl** out);
 int grid_leaf_codes(const GridImpl* g, uint64_t first, uint64_t count, uint8_t* codes, float* params);
+int quantise_svdb(const uint8_t* svdb, size_t n, int codec, int device, std::vector<uint8_t>& out);
 int read_voxels_device(const GridImpl* g, const int32_t* d_ijk, size_t n, float* d_out, cudaStream_t s);
 int sample_device(const GridImpl* g, const double* d_xyz, size_t n, int mode, float* d_out, cudaStream_t s);
 int gradient_device(const GridImpl* g, const double* d_xyz, size_t n, double* d_out, cudaStream_t s);

@@ -101,8 +101,12 @@ def test_corrupt_svdb_rejected_before_touching_the_device():
         P.DeviceGrid(b"XVDB" + bytes(100))
     assert e.value.code == P.Errc.bad_magic
     with pytest.raises(P.Error) as e:
-        P.DeviceGrid(b"SVDB" + (2).to_bytes(4, "little") + bytes(100))
+        P.DeviceGrid(b"SVDB" + (3).to_bytes(4, "little") + bytes(100))
     assert e.value.code == P.Errc.version_mismatch
+    # version 2 is the quantised container: its header is validated like v1's
+    with pytest.raises(P.Error) as e:
+        P.DeviceGrid(b"SVDB" + (2).to_bytes(4, "little") + bytes(100))
+    assert e.value.code == P.Errc.corrupt_index
 
 
 def test_scene_table_covers_baseline_configs():
