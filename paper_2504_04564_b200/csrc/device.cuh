@@ -76,6 +76,9 @@ __device__ __forceinline__ int find_upper(const DevGrid& g, int ox, int oy, int 
 
 // Per-thread read-through cache (Accessor, frozen.hpp:228-277). Keys are the coordinate-derived
 // node origins; values never depend on the cache state (test_tree.cpp:247-271).
+#ifndef SVDB_LEAF_DIR
+#define SVDB_LEAF_DIR 1
+#endif
 template <int CODEC>
 struct Accessor {
     const DevGrid* g;
@@ -166,6 +169,26 @@ struct Accessor {
     {
         if (in_leaf(x, y, z))
             return true;
+#if SVDB_LEAF_DIR
+        if (g->dir) {
+            const unsigned cx = unsigned(x) >> 3, cy = unsigned(y) >> 3, cz = unsigned(z) >> 3;
+            if (x >= 0 && y >= 0 && z >= 0 && cx < unsigned(g->dir_dims[0]) && cy < unsigned(g->dir_dims[1]) &&
+                cz < unsigned(g->dir_dims[2])) {
+                const uint4 e = __ldg(g->dir + (size_t(cz) * unsigned(g->dir_dims[1]) + cy) * unsigned(g->dir_dims[0]) + cx);
+                if (e.x != kSlotChild) {
+                    value = __uint_as_float(e.y); // tile value, or the background stored as one
+                    return false;
+                }
+                lx = x & ~7;
+                ly = y & ~7;
+                lz = z & ~7;
+                leaf = e.y;
+                lo = __uint_as_float(e.z);
+                sc = __uint_as_float(e.w);
+                return true;
+            }
+        }
+#endif
         if (!in_lower(x, y, z)) {
             const int ox = x & ~4095, oy = y & ~4095, oz = z & ~4095;
             if (!(ox == ux && oy == uy && oz == uz)) {

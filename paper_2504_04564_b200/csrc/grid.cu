@@ -187,6 +187,17 @@ __device__ uint4 resolve_block(const DevGrid& g, int x, int y, int z)
     return bg;
 }
 
+// Leaf directory build: one thread per 8^3 block, the same resolution as the apron build
+__global__ void k_build_dir(DevGrid g, int3 dd, uint4* __restrict__ dir)
+{
+    const uint64_t n = uint64_t(dd.x) * dd.y * dd.z;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const int cx = int(i % uint64_t(dd.x)), cy = int((i / uint64_t(dd.x)) % uint64_t(dd.y)),
+                  cz = int(i / (uint64_t(dd.x) * dd.y));
+        dir[i] = resolve_block(g, 8 * cx, 8 * cy, 8 * cz);
+    }
+}
+
 template <int CODEC>
 __global__ void __launch_bounds__(256) k_build_apron(DevGrid g, const int4* __restrict__ lorg, uint64_t n_leaf,
                                                      const float2* __restrict__ own, int* __restrict__ bad)
@@ -368,6 +379,7 @@ GridImpl::~GridImpl()
     cudaFree(d_maj);
     cudaFree(d_inv_maj);
     cudaFree(d_inv_maj_f);
+    cudaFree(d_dir);
     cudaFree(d_tf);
     cudaFree(d_img);
     cudaFree(d_counters);
@@ -695,6 +707,24 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
     g->leaf_payload_bytes = uint64_t(stride) * nf + 64 * nf;
     g->device_bytes = sizeof(int4) * h_root.size() + sizeof(uint2) * h_upper.size() + sizeof(uint4) * h_lower.size() +
                       uint64_t(stride) * nf + 64 * nf;
+    // leaf directory over the grid's box, when it costs at most 1 GiB or no more than the lower table
+    {
+        const int3 dd = make_int3((dims[0] + 7) / 8, (dims[1] + 7) / 8, (dims[2] + 7) / 8);
+        const uint64_t nd = uint64_t(dd.x) * dd.y * dd.z, bytes = nd * sizeof(uint4);
+        if (nd && (bytes <= (1ull << 30) || bytes <= sizeof(uint4) * h_lower.size()) &&
+            cudaMalloc(&g->d_dir, bytes) == cudaSuccess) {
+            k_build_dir<<<grid_blocks(nd), 256, 0, s>>>(g->dg, dd, g->d_dir);
+            SVDB_CUDA(cudaGetLastError());
+            SVDB_CUDA(cudaStreamSynchronize(s));
+            g->dg.dir = g->d_dir;
+            g->dg.dir_dims[0] = dd.x;
+            g->dg.dir_dims[1] = dd.y;
+            g->dg.dir_dims[2] = dd.z;
+            g->device_bytes += bytes;
+        } else {
+            cudaGetLastError(); // an over-budget or failed allocation just means no directory
+        }
+    }
     *out = g.release();
     return 0;
 }

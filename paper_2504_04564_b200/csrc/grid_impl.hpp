@@ -35,6 +35,7 @@ struct GridImpl {
     uint4* d_lower = nullptr;
     uint8_t* d_codes = nullptr;
     float2* d_lparams = nullptr;
+    uint4* d_dir = nullptr; // leaf directory (DevGrid::dir)
     uint64_t device_bytes = 0, leaf_payload_bytes = 0;
 
     // macrocells: exact closed-box ranges cached per grid (macrocell.hpp:74-103);

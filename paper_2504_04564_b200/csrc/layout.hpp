@@ -25,6 +25,11 @@ struct DevGrid {
     float2* lparams;      // 8 x (lo, scale) per leaf: [0] own, [1..7] apron regions
     uint32_t leaf_stride; // bytes per leaf: own block (main_bytes) + 217-entry apron
     uint32_t main_bytes;  // 2048 f32, 512 u8, 256 u4
+    // leaf directory: for every 8^3 block of [0, 8*dir_dims) the root->upper->lower walk resolved
+    // at build time ({kind, payload, lo, scale} as in `lower`; tile / background as kind tile with
+    // the value). One load replaces the node walk for in-box lookups; null when over budget.
+    const uint4* dir;
+    int dir_dims[3];
 };
 
 struct DevTF {

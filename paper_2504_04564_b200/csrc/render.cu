@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
 #endif
     double t = 0.0, tb = 0.0, inv = 0.0;
 #ifdef SVDB_PHASE_STATS
-    unsigned st_empty = 0, st_full = 0;
+    unsigned st_empty = 0, st_full = 0, st_leaf_hit = 0, st_lower_hit = 0;
 #endif
 #if SVDB_MAJ_AHEAD
     double inv_ahead = 0.0;
@@ -1018,6 +1018,17 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
 #if SVDB_ACC_SHARED
         acc_io(false);
 #endif
+#ifdef SVDB_PHASE_STATS
+        {
+            const Ray rr = ray_load();
+            const int qx = lattice_coord(rr.o[0] + rr.d[0] * t), qy = lattice_coord(rr.o[1] + rr.d[1] * t),
+                      qz = lattice_coord(rr.o[2] + rr.d[2] * t);
+            if (tr.acc.in_leaf(qx, qy, qz))
+                ++st_leaf_hit;
+            else if (tr.acc.in_lower(qx, qy, qz))
+                ++st_lower_hit;
+        }
+#endif
         float v = tr.sample_at(ray_load(), t);
 #if SVDB_ACC_SHARED
         acc_io(true);
@@ -1156,6 +1167,8 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
 #ifdef SVDB_PHASE_STATS
     atomicAdd(A.counters + 12, (unsigned long long)st_empty); // macrocell visits: empty / non-empty
     atomicAdd(A.counters + 13, (unsigned long long)st_full);
+    atomicAdd(A.counters + 14, (unsigned long long)st_leaf_hit); // gathers: leaf-cache hits
+    atomicAdd(A.counters + 15, (unsigned long long)st_lower_hit); // leaf miss, lower-cache hit
 #endif
 }
 
@@ -1352,6 +1365,8 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         cudaMemcpy(c, g->d_counters, 128, cudaMemcpyDeviceToHost);
         const char* names[3] = {"start", "advance", "gather"};
         fprintf(stderr, "[phase-stats] macrocell visits: empty %llu non-empty %llu\n", c[12], c[13]);
+        fprintf(stderr, "[phase-stats] gathers %llu: leaf-cache hits %llu, lower-cache hits %llu\n", samples, c[14],
+                c[15]);
         for (int p = 0; p < 3; ++p)
             fprintf(stderr, "[phase-stats] %-8s invocations %llu lanes/invocation %.2f cycles/invocation %.1f\n",
                     names[p], c[2 + 2 * p], c[2 + 2 * p] ? double(c[3 + 2 * p]) / double(c[2 + 2 * p]) : 0.0,

@@ -138,7 +138,7 @@ def test_svdb_errors_map_to_errc(gpu, ref):
     with pytest.raises(P.Error) as e:
         P.DeviceGrid(bytes(bad))
     assert e.value.code == P.Errc.bad_magic
-    bad = bytearray(svdb); bad[4] = 2
+    bad = bytearray(svdb); bad[4] = 3  # (2 is the quantised container, test_gpu_quantised.py)
     with pytest.raises(P.Error) as e:
         P.DeviceGrid(bytes(bad))
     assert e.value.code == P.Errc.version_mismatch
