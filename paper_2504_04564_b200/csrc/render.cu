@@ -682,6 +682,9 @@ struct DdaRegs {
 #ifndef SVDB_ACC_SHARED
 #define SVDB_ACC_SHARED 1
 #endif
+#ifndef SVDB_ACC_DIR_COLD
+#define SVDB_ACC_DIR_COLD 0
+#endif
 template <int CODEC, int MODE>
 __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
 {
@@ -1016,7 +1019,14 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         ++tr.samples;
 #else
 #if SVDB_ACC_SHARED
-        acc_io(false);
+#if SVDB_ACC_DIR_COLD
+        // with a leaf directory every leaf-cache miss is one load: start each gather from a cold
+        // accessor instead of saving / restoring its 14 words (the leaf cache hits ~5% in C3)
+        if (A.g.dir)
+            tr.acc = Accessor<CODEC>(A.g);
+        else
+#endif
+            acc_io(false);
 #endif
 #ifdef SVDB_PHASE_STATS
         {
@@ -1031,7 +1041,10 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
 #endif
         float v = tr.sample_at(ray_load(), t);
 #if SVDB_ACC_SHARED
-        acc_io(true);
+#if SVDB_ACC_DIR_COLD
+        if (!A.g.dir)
+#endif
+            acc_io(true);
 #endif
 #endif
         accept(v);
