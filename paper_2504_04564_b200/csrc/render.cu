@@ -727,8 +727,16 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
 #if SVDB_ACC_SHARED
     // the accessor's node caches (frozen.hpp:228-277) are used only by the gather: shared memory
     // between gathers, registers inside one
-    __shared__ int s_acc[14][SVDB_TRACE_THREADS];
+    // Ratio tracking keeps no accessor state between gathers (the leaf directory makes a cold
+    // locate one load): its extra per-lane state would otherwise cap it at 10 CTAs per SM.
+    constexpr bool PERSIST_ACC = !RATIO;
+    __shared__ int s_acc[PERSIST_ACC ? 14 : 1][SVDB_TRACE_THREADS];
     auto acc_io = [&](bool store) {
+        if constexpr (!PERSIST_ACC) {
+            if (!store)
+                tr.acc = Accessor<CODEC>(A.g);
+            return;
+        }
         volatile int* p = &s_acc[0][threadIdx.x];
         int* f[14] = {&tr.acc.lx, &tr.acc.ly, &tr.acc.lz, reinterpret_cast<int*>(&tr.acc.leaf),
                       reinterpret_cast<int*>(&tr.acc.lo), reinterpret_cast<int*>(&tr.acc.sc),
@@ -766,8 +774,8 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
     // Per-lane state touched only at sample start/end, scatter and pixel output lives in shared
     // memory (SoA, conflict-free), keeping the step/gather loop's register footprint small.
     __shared__ double s_cold_d[7][SVDB_TRACE_THREADS];
-    __shared__ double s_ratio_d[RATIO ? 5 : 1][SVDB_TRACE_THREADS]; // ratio tracking only
-    __shared__ int s_cold_i[6][SVDB_TRACE_THREADS];
+    __shared__ double s_ratio_d[RATIO ? 4 : 1][SVDB_TRACE_THREADS]; // ratio tracking only
+    __shared__ int s_cold_i[RATIO ? 7 : 6][SVDB_TRACE_THREADS];
     const int tid = threadIdx.x;
     volatile double &acc0 = s_cold_d[0][tid], &acc1 = s_cold_d[1][tid], &acc2 = s_cold_d[2][tid];
     volatile double &tp0 = s_cold_d[3][tid], &tp1 = s_cold_d[4][tid], &tp2 = s_cold_d[5][tid];
@@ -775,14 +783,14 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
     constexpr int kR = RATIO ? 1 : 0; // pathtrace: the ratio names alias one unused row
     volatile double &L0 = s_ratio_d[0][tid], &L1 = s_ratio_d[kR][tid], &L2 = s_ratio_d[2 * kR][tid];
     volatile double &Tr = s_ratio_d[3 * kR][tid];
-    volatile double& have_d = s_ratio_d[4 * kR][tid]; // ratio: event pending (0/1)
+    volatile int& have_d = s_cold_i[RATIO ? 6 : 0][tid]; // ratio: event pending (0/1)
     volatile int &px = s_cold_i[0][tid], &py = s_cold_i[1][tid], &s = s_cold_i[2][tid];
     volatile int &bounces = s_cold_i[3][tid], &out_off = s_cold_i[4][tid];
     volatile float& v_ev = reinterpret_cast<volatile float&>(s_cold_i[5][tid]);
     struct HaveRef {
-        volatile double& d;
-        __device__ operator bool() const { return d != 0.0; }
-        __device__ HaveRef& operator=(bool b) { d = b ? 1.0 : 0.0; return *this; }
+        volatile int& d;
+        __device__ operator bool() const { return d != 0; }
+        __device__ HaveRef& operator=(bool b) { d = b ? 1 : 0; return *this; }
     } have{have_d};
     acc0 = acc1 = acc2 = 0.0;
     tp0 = tp1 = tp2 = 1.0;

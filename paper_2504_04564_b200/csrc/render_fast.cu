@@ -279,7 +279,10 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
     SharedDdaG<G> dda{&s_dda_i[0][0], &s_dda_f[0][0], tid};
     __shared__ G s_ray[6][kT];
     __shared__ G s_tev[kT];
-    __shared__ int s_acc[14][kT];
+    // ratio tracking keeps no accessor state between gathers (cold locate = one directory load):
+    // its extra per-lane state would otherwise cost CTAs per SM
+    constexpr bool PERSIST_ACC = !RATIO;
+    __shared__ int s_acc[PERSIST_ACC ? 14 : 1][kT];
     __shared__ double s_sum[3][kT];                    // per-pixel FP64 accumulation
     __shared__ float s_cold[RATIO ? 8 : 5][kT];        // tp0..2, (unused), v_ev (+ L0..2)
     // ratio transmittance stays FP64: a float product underflows to 0 (ending the flight) long
@@ -299,6 +302,11 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
 
     Accessor<CODEC> acc(A.g);
     auto acc_io = [&](bool store) {
+        if constexpr (!PERSIST_ACC) {
+            if (!store)
+                acc = Accessor<CODEC>(A.g);
+            return;
+        }
         volatile int* p = &s_acc[0][tid];
         int* f[14] = {&acc.lx, &acc.ly, &acc.lz, reinterpret_cast<int*>(&acc.leaf), reinterpret_cast<int*>(&acc.lo),
                       reinterpret_cast<int*>(&acc.sc), &acc.wx, &acc.wy, &acc.wz, reinterpret_cast<int*>(&acc.lower),
