@@ -33,6 +33,13 @@ sys.path.insert(0, ROOT)
 
 SECTOR_BYTES = 32  # algorithmic bytes per lookup (one HBM sector per random tap), SURVEY.md §8d
 L2_BYTES = 126 << 20  # B200 L2
+METRIC = "Mpaths/s (1024^3 8-bit compressed VDB path tracing; Mlookups/s alongside)"
+
+
+def workload(sc):
+    return (f"{sc.name}: {sc.dims[0]}x{sc.dims[1]}x{sc.dims[2]} {sc.volume} -> {sc.codec.name} leaves, "
+            f"{sc.width}x{sc.height}, {sc.settings.spp} spp, {sc.settings.mode.name}, "
+            f"max_bounces {sc.settings.max_bounces}")
 L2_FLUSH_BYTES = 256 << 20  # written between timed steps when the leaf payload fits in L2
 
 
@@ -217,11 +224,11 @@ def run_reference_arm(args):
         res = r
     value = statistics.median([r["value"] for r in times]) if times else res["value"]
     line = {
-        "impl": "reference", "metric": "Mpaths/s (1024^3 8-bit compressed VDB path tracing)", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "Mpaths/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{sc.name}: {sc.dims[0]}^3 {sc.volume} {sc.codec.name} leaves, "
-                               f"{sc.width}x{sc.height}, {sc.settings.spp} spp, {sc.settings.mode.name}"},
+        "config": {"workload": workload(sc), "timed": "the unmodified reference's render_field body on "
+                                                         "the host (oracle/_ref), bounded tile samples"},
         "mlookups_per_s": statistics.median([r["mlookups_per_s"] for r in times]) if times else None,
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": value, "unit": "Mpaths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -402,13 +409,11 @@ def run_ours(args):
                          if args.scale == 1 and args.kernel == 0 and not args.mode
                          and args.majorant_cell in (0, 32) and args.precision == "fp64" else (None, None))
         line = {
-            "metric": "Mpaths/s (1024^3 8-bit compressed VDB path tracing; Mlookups/s alongside)",
+            "metric": METRIC,
             "value": value, "unit": "Mpaths/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": ["f64", "f32", "f64/f32"][sc.settings.precision], "data": "synthetic",
-            "config": {"workload": f"{sc.name}: {sc.dims[0]}x{sc.dims[1]}x{sc.dims[2]} {sc.volume} -> "
-                                   f"{grid.codec.name} leaves, {sc.width}x{sc.height}, {sc.settings.spp} spp, "
-                                   f"{sc.settings.mode.name}, max_bounces {sc.settings.max_bounces}",
+            "config": {"workload": workload(sc),
                        "majorant_cell": sc.settings.majorant_cell or 32,
                        "image_split": f"interleaved 16x16 tiles over {world} GPU(s), NCCL gather to rank 0",
                        "l2": (f"L2 flushed between timed steps ({L2_FLUSH_BYTES >> 20} MB write outside the "
