@@ -637,7 +637,7 @@ struct DdaRegs {
 #define SVDB_TRACE_THREADS 64 // 2 warps per CTA, <= 80 registers: 24 resident warps per SM
 #endif
 #ifndef SVDB_TRACE_MIN_BLOCKS
-#define SVDB_TRACE_MIN_BLOCKS 12
+#define SVDB_TRACE_MIN_BLOCKS 14 // <= 72 registers, 14.6 KB shared: 28 resident warps per SM
 #endif
 #ifndef SVDB_SCHED
 #define SVDB_SCHED 1 // 0: advance-to-point then gather; 1: per-iteration phase selection
@@ -681,6 +681,9 @@ struct DdaRegs {
 #endif
 #ifndef SVDB_ACC_SHARED
 #define SVDB_ACC_SHARED 1
+#endif
+#ifndef SVDB_PERSIST_ACC_PT
+#define SVDB_PERSIST_ACC_PT 0 // 1: pathtrace keeps the accessor's caches between gathers
 #endif
 #ifndef SVDB_ACC_DIR_COLD
 #define SVDB_ACC_DIR_COLD 0
@@ -727,9 +730,10 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
 #if SVDB_ACC_SHARED
     // the accessor's node caches (frozen.hpp:228-277) are used only by the gather: shared memory
     // between gathers, registers inside one
-    // Ratio tracking keeps no accessor state between gathers (the leaf directory makes a cold
-    // locate one load): its extra per-lane state would otherwise cap it at 10 CTAs per SM.
-    constexpr bool PERSIST_ACC = !RATIO;
+    // No accessor state is kept between gathers: with the leaf directory a cold locate is one load
+    // (the leaf cache hit only ~5% of gathers), and dropping the 14 words per lane of shared memory
+    // and their registers lets 14 CTAs (28 warps) fit per SM instead of 12 (10 for ratio).
+    constexpr bool PERSIST_ACC = !RATIO && SVDB_PERSIST_ACC_PT;
     __shared__ int s_acc[PERSIST_ACC ? 14 : 1][SVDB_TRACE_THREADS];
     auto acc_io = [&](bool store) {
         if constexpr (!PERSIST_ACC) {

@@ -36,13 +36,16 @@ namespace {
 
 constexpr int kT = 64;          // threads per CTA
 #ifndef SVDB_F_MIN_BLOCKS_MIXED
-#define SVDB_F_MIN_BLOCKS_MIXED 12
+#define SVDB_F_MIN_BLOCKS_MIXED 14
+#endif
+#ifndef SVDB_F_PERSIST_ACC
+#define SVDB_F_PERSIST_ACC 0 // accessor caches kept between gathers (off: cold locate = one directory load)
 #endif
 #ifndef SVDB_F_ADV_ITERS
 #define SVDB_F_ADV_ITERS 3
 #endif
 constexpr int kMinBlocks = 16;                           // 32 warps per SM (pure FP32)
-constexpr int kMinBlocksMixed = SVDB_F_MIN_BLOCKS_MIXED; // FP64 geometry: 264 B of shared state per lane
+constexpr int kMinBlocksMixed = SVDB_F_MIN_BLOCKS_MIXED; // FP64 geometry: 212 B of shared state per lane
 constexpr int kAdvIters = SVDB_F_ADV_ITERS;              // advance steps per advance-phase invocation
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -279,9 +282,9 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
     SharedDdaG<G> dda{&s_dda_i[0][0], &s_dda_f[0][0], tid};
     __shared__ G s_ray[6][kT];
     __shared__ G s_tev[kT];
-    // ratio tracking keeps no accessor state between gathers (cold locate = one directory load):
-    // its extra per-lane state would otherwise cost CTAs per SM
-    constexpr bool PERSIST_ACC = !RATIO;
+    // no accessor state between gathers (cold locate = one directory load): its per-lane state
+    // would otherwise cost CTAs per SM
+    constexpr bool PERSIST_ACC = SVDB_F_PERSIST_ACC != 0;
     __shared__ int s_acc[PERSIST_ACC ? 14 : 1][kT];
     __shared__ double s_sum[3][kT];                    // per-pixel FP64 accumulation
     __shared__ float s_cold[RATIO ? 8 : 5][kT];        // tp0..2, (unused), v_ev (+ L0..2)
