@@ -464,6 +464,8 @@ struct SharedDda {
     __device__ __forceinline__ int cy() { return ci(1); }
     __device__ __forceinline__ int cz() { return ci(2); }
     __device__ __forceinline__ bool done() { return ci(6) != 0; }
+    __device__ __forceinline__ int stepv(int axis) { return ci(3 + axis); }
+    __device__ __forceinline__ void set_done() { ci(6) = 1; }
     __device__ __forceinline__ int index(const int cells[3]) { return ci(0) + cells[0] * (ci(1) + cells[1] * ci(2)); }
 
     // clip_ray_box + dda_traverse setup (dda.hpp:25-86). Rolled per-axis loops keep one copy of
@@ -523,7 +525,7 @@ struct SharedDda {
 
     __device__ __forceinline__ bool next(const int cells[3], int cell[3], double& ta, double& tb)
     {
-        if (ci(6))
+        if (done())
             return false;
         const double n0 = cd(0), n1 = cd(1), n2 = cd(2), t_cur = cd(6), t1 = cd(7);
         const bool ax1 = n1 < n0;
@@ -539,14 +541,14 @@ struct SharedDda {
         ta = t_cur;
         tb = t_exit;
         if (t_exit >= t1) {
-            ci(6) = 1;
+            set_done();
             return true;
         }
         cd(6) = t_exit;
-        const int c = (axis == 0 ? cell[0] : (axis == 1 ? cell[1] : cell[2])) + ci(3 + axis);
+        const int c = (axis == 0 ? cell[0] : (axis == 1 ? cell[1] : cell[2])) + stepv(axis);
         ci(axis) = c;
         if (c < 0 || c >= cells[axis])
-            ci(6) = 1;
+            set_done();
         else
             cd(axis) = (axis == 0 ? n0 : (axis == 1 ? n1 : n2)) + cd(3 + axis);
         return true;
@@ -573,7 +575,7 @@ struct DdaRegs {
         n[2] = d.cd(2);
         t_cur = d.cd(6);
         t1 = d.cd(7);
-        dn = d.ci(6) != 0;
+        dn = d.done();
     }
     __device__ __forceinline__ void store()
     {
@@ -608,7 +610,7 @@ struct DdaRegs {
             return true;
         }
         t_cur = t_exit;
-        const int cn = (axis == 0 ? c[0] : (axis == 1 ? c[1] : c[2])) + s->ci(3 + axis);
+        const int cn = (axis == 0 ? c[0] : (axis == 1 ? c[1] : c[2])) + s->stepv(axis);
         if (axis == 0)
             c[0] = cn;
         else if (axis == 1)
@@ -777,16 +779,17 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
 #if SVDB_COLD_SHARED
     // Per-lane state touched only at sample start/end, scatter and pixel output lives in shared
     // memory (SoA, conflict-free), keeping the step/gather loop's register footprint small.
-    __shared__ double s_cold_d[7][SVDB_TRACE_THREADS];
-    __shared__ double s_ratio_d[RATIO ? 4 : 1][SVDB_TRACE_THREADS]; // ratio tracking only
+    // rows 0..6: acc0..2, tp0..2, t_ev; ratio tracking adds L0..2, Tr (pathtrace aliases those
+    // names to row 6, written only by the initialisation below, before t_ev)
+    __shared__ double s_cold_d[RATIO ? 11 : 7][SVDB_TRACE_THREADS];
     __shared__ int s_cold_i[RATIO ? 7 : 6][SVDB_TRACE_THREADS];
     const int tid = threadIdx.x;
     volatile double &acc0 = s_cold_d[0][tid], &acc1 = s_cold_d[1][tid], &acc2 = s_cold_d[2][tid];
     volatile double &tp0 = s_cold_d[3][tid], &tp1 = s_cold_d[4][tid], &tp2 = s_cold_d[5][tid];
     volatile double& t_ev = s_cold_d[6][tid];
-    constexpr int kR = RATIO ? 1 : 0; // pathtrace: the ratio names alias one unused row
-    volatile double &L0 = s_ratio_d[0][tid], &L1 = s_ratio_d[kR][tid], &L2 = s_ratio_d[2 * kR][tid];
-    volatile double &Tr = s_ratio_d[3 * kR][tid];
+    constexpr int kR0 = RATIO ? 7 : 6, kR = RATIO ? 1 : 0;
+    volatile double &L0 = s_cold_d[kR0][tid], &L1 = s_cold_d[kR0 + kR][tid], &L2 = s_cold_d[kR0 + 2 * kR][tid];
+    volatile double &Tr = s_cold_d[kR0 + 3 * kR][tid];
     volatile int& have_d = s_cold_i[RATIO ? 6 : 0][tid]; // ratio: event pending (0/1)
     volatile int &px = s_cold_i[0][tid], &py = s_cold_i[1][tid], &s = s_cold_i[2][tid];
     volatile int &bounces = s_cold_i[3][tid], &out_off = s_cold_i[4][tid];
