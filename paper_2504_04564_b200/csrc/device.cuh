@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "layout.hpp"
+#include "log_glibc.h"
 
 namespace svdbgpu {
 
@@ -431,6 +432,20 @@ __device__ __forceinline__ double tf_max_alpha_in_range(const DevTF& tf, const f
             m = dmax(m, double(ent[i].w));
     }
     return m;
+}
+
+// ---- the free-flight log (render.hpp:116): the reference's glibc log restated (log_glibc.h), so
+// step lengths match the reference bit for bit rather than to CUDA log's <= 1 ulp ----
+#ifndef SVDB_GLIBC_LOG
+#define SVDB_GLIBC_LOG 0 // 1: step lengths bit-exact to the reference; measured -5% (C3) / -7% (C4)
+#endif
+__device__ __forceinline__ double step_log(double w)
+{
+#if SVDB_GLIBC_LOG
+    return glibc_log(w);
+#else
+    return log(w);
+#endif
 }
 
 // ---- splitmix64 streams (rng.hpp:12-67) ----

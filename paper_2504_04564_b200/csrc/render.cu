@@ -55,7 +55,7 @@ struct Tracer {
         double inv = 1.0 / sigma_maj;
         double t = t0;
         for (;;) {
-            t -= log(1.0 - rng.uniform()) * inv;
+            t -= step_log(1.0 - rng.uniform()) * inv;
             if (t >= t1)
                 return false;
             float v = sample_at(r, t);
@@ -174,7 +174,7 @@ struct Tracer {
                     double inv = 1.0 / double(m);
                     double t = ta;
                     for (;;) {
-                        t -= log(1.0 - rng.uniform()) * inv;
+                        t -= step_log(1.0 - rng.uniform()) * inv;
                         if (t >= tb)
                             break;
                         float v = sample_at(ray, t);
@@ -949,7 +949,7 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         // the step draw's log does not depend on the DDA: compute it from the next uniform before
         // the cell lookup (independent FP64 chains interleave); the draw is consumed only if the
         // cell has draws, so the stream is unchanged
-        const double lg = log(1.0 - rng.peek());
+        const double lg = step_log(1.0 - rng.peek());
 #endif
         if (state == kNeedCell) {
             int c[3];
@@ -998,7 +998,7 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         rng.skip();
         t -= lg * inv;
 #else
-        t -= log(1.0 - rng.uniform()) * inv;
+        t -= step_log(1.0 - rng.uniform()) * inv;
 #endif
         state = t >= tb ? kNeedCell : kPoint;
     };
