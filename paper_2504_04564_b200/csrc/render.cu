@@ -675,9 +675,6 @@ struct DdaRegs {
 #ifndef SVDB_MAJ_AHEAD
 #define SVDB_MAJ_AHEAD 1
 #endif
-#ifndef SVDB_DDA_SHARED
-#define SVDB_DDA_SHARED 1
-#endif
 #ifndef SVDB_RAY_SHARED
 #define SVDB_RAY_SHARED 1
 #endif
@@ -758,17 +755,11 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
     };
     acc_io(true);
 #endif
-#if SVDB_DDA_SHARED
+    // macrocell DDA state (23 words per lane) in shared memory, touched once per cell visit
     __shared__ int s_dda_i[7][SVDB_TRACE_THREADS];
     __shared__ double s_dda_d[8][SVDB_TRACE_THREADS];
     SharedDda<SVDB_TRACE_THREADS> dda{&s_dda_i[0][0], &s_dda_d[0][0], int(threadIdx.x)};
-    auto dda_cur_index = [&]() { return dda.cx() + A.cells[0] * (dda.cy() + A.cells[1] * dda.cz()); };
-    auto dda_done = [&]() { return dda.done(); };
-#else
-    Dda dda;
-    auto dda_cur_index = [&]() { return tr.cell_index(dda.c); };
-    auto dda_done = [&]() { return dda.done; };
-#endif
+    auto dda_cur_index = [&]() { return dda.index(A.cells); };
     double t = 0.0, tb = 0.0, inv = 0.0;
 #ifdef SVDB_PHASE_STATS
     unsigned st_empty = 0, st_full = 0, st_leaf_hit = 0, st_lower_hit = 0;
