@@ -9,6 +9,7 @@
 #include "grid_impl.hpp"
 
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -711,7 +712,8 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
     {
         const int3 dd = make_int3((dims[0] + 7) / 8, (dims[1] + 7) / 8, (dims[2] + 7) / 8);
         const uint64_t nd = uint64_t(dd.x) * dd.y * dd.z, bytes = nd * sizeof(uint4);
-        if (nd && (bytes <= (1ull << 30) || bytes <= sizeof(uint4) * h_lower.size()) &&
+        const char* off = std::getenv("SVDBGPU_NO_LEAF_DIR"); // diagnostics: force the node walk
+        if (nd && !(off && off[0] == '1') && (bytes <= (1ull << 30) || bytes <= sizeof(uint4) * h_lower.size()) &&
             cudaMalloc(&g->d_dir, bytes) == cudaSuccess) {
             k_build_dir<<<grid_blocks(nd), 256, 0, s>>>(g->dg, dd, g->d_dir);
             SVDB_CUDA(cudaGetLastError());

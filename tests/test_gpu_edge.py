@@ -108,3 +108,22 @@ def test_far_positions_sample_background(gpu, ref):
     got = g.sample(xyz)
     want = ref.open(svdb).sample(xyz)
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_node_walk_without_leaf_directory_is_identical(gpu, ref, monkeypatch):
+    # grids whose leaf directory would exceed its budget fall back to the root/upper/lower walk
+    # (SVDBGPU_NO_LEAF_DIR forces it): same voxels, samples and images bit for bit
+    from helpers import all_coords, bits
+    svdb = _tile_grid(ref, dims=(70, 45, 33), background=0.3, seed=11)
+    with_dir = P.DeviceGrid(svdb, P.Codec.affine8)
+    monkeypatch.setenv("SVDBGPU_NO_LEAF_DIR", "1")
+    no_dir = P.DeviceGrid(svdb, P.Codec.affine8)
+    assert no_dir.device_bytes < with_dir.device_bytes
+    ijk = all_coords((-2, -2, -2), (73, 48, 36))
+    assert np.array_equal(bits(with_dir.read_voxels(ijk)), bits(no_dir.read_voxels(ijk)))
+    cam = P.Camera(position=(140.0, 90.0, -60.0), look_at=(35.0, 22.0, 16.0), fov_y_deg=40.0, width=53, height=37)
+    for mode in (P.RenderMode.pathtrace, P.RenderMode.ratio, P.RenderMode.ea):
+        st = P.RenderSettings(spp=8, seed=5, mode=mode)
+        a = P.render(with_dir, TF, cam, st).pixels
+        b = P.render(no_dir, TF, cam, st).pixels
+        assert np.array_equal(bits(a), bits(b))
