@@ -1,15 +1,22 @@
-// render.cu — the path-tracing megakernel (K4) and the north-star integrators (K5 EA, K6 ratio),
-// plus the ISO marcher. One thread per pixel; each CTA is one 16x16 image tile (the reference's
-// tile, render.hpp:285-313), each warp an 8x4 pixel block so primary rays stay coherent.
-// Samples of a pixel run in index order and accumulate in FP64 (render.hpp:297-310), so the
-// image is independent of the launch shape and of how tiles are split across ranks/GPUs.
+// render.cu — the reference-exact (FP64) render kernels and the render() entry point.
 //
-//   render_field  render.hpp:276-315   -> k_render
-//   camera_ray    render.hpp:259-269   -> host basis (exact) + camera_dir
-//   trace_path    render.hpp:160-187   -> trace_path
-//   next_event    render.hpp:137-151   -> next_event
-//   woodcock_track render.hpp:106-124  -> woodcock
-//   trace_iso     render.hpp:193-255   -> trace_iso
+//   k_trace  (pathtrace K4, ratio K6): persistent, path-regenerating tracer. Every lane is a small
+//            state machine over its own pixels; each loop iteration runs the phase (start /
+//            advance / gather) most lanes of the warp are waiting in. Per-lane state lives in
+//            shared memory between phases; 71 registers, 28 warps per SM.
+//   k_render (EA K5, ISO, and the per-pixel A/B baseline): one thread per pixel, a CTA per 16x16
+//            image tile (the reference's tile, render.hpp:285-313), each warp an 8x4 pixel block.
+//   render() sets up majorants, launches one of them (or render_fast.cu's FP32-arithmetic tracer)
+//            and reports stats.
+// Samples of a pixel run in index order and accumulate in FP64 (render.hpp:297-310) in both
+// kernels, so the image is independent of the launch shape and of how tiles are split over GPUs.
+//
+//   render_field  render.hpp:276-315   -> k_trace / k_render
+//   camera_ray    render.hpp:259-269   -> host basis (exact) + camera_ray
+//   trace_path    render.hpp:160-187   -> k_trace state machine (Tracer::trace_path in k_render)
+//   next_event    render.hpp:137-151   -> SharedDda + do_advance (Tracer::next_event)
+//   woodcock_track render.hpp:106-124  -> do_advance + accept (Tracer::woodcock)
+//   trace_iso     render.hpp:193-255   -> Tracer::trace_iso
 #include "device.cuh"
 #include "grid_impl.hpp"
 #include "render_args.hpp"
