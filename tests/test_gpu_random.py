@@ -71,3 +71,20 @@ def test_random_samples_bit_exact(gpu, ref, seed):
     got = g.sample(xyz)
     want = ref.open(svdb).sample(xyz)
     assert np.array_equal(bits(got), bits(want))
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_quantised_scene_parity(gpu, ref, orc, seed):
+    # N-bit leaves: the oracle image is the reference on the dequantised SVDB
+    svdb, tf, cam, st = _random_case(ref, 3000 + seed)
+    codec = P.Codec.affine8 if seed % 2 == 0 else P.Codec.affine4
+    g = P.DeviceGrid(svdb, codec)
+    deq, _, _ = orc.quantize(svdb, int(codec))
+    img = P.render(g, tf, cam, st).pixels
+    if st.mode in (P.RenderMode.pathtrace, P.RenderMode.iso):
+        want = ref.open(deq).render(tf, cam, st)
+    else:
+        want, _, _ = orc.open(deq).render(tf, cam, st)
+    same, rmse = image_parity(img, want)
+    print(f"seed {seed} {codec.name} {st.mode.name}: identical {same:.4f} rmse {rmse:.2e}")
+    assert rmse <= 1e-3 and same >= 0.98
