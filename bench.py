@@ -226,7 +226,7 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value,
         "unit": "Mpaths/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload(sc), "timed": "the unmodified reference's render_field body on "
                                                          "the host (oracle/_ref), bounded tile samples"},
         "mlookups_per_s": statistics.median([r["mlookups_per_s"] for r in times]) if times else None,
@@ -411,7 +411,7 @@ def run_ours(args):
         line = {
             "metric": METRIC,
             "value": value, "unit": "Mpaths/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": ["f64", "f32", "f64/f32"][sc.settings.precision], "data": "synthetic",
             "config": {"workload": workload(sc),
                        "majorant_cell": sc.settings.majorant_cell or 32,
