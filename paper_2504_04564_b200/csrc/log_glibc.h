@@ -25,7 +25,7 @@
 
 namespace svdbgpu {
 
-struct LogTabEntry {
+struct alignas(16) LogTabEntry {
     double invc, logc;
 };
 
@@ -85,7 +85,8 @@ SVDB_HD double glibc_log(double x)
     const int k = int(static_cast<int64_t>(tmp) >> 52);
     const uint64_t iz = ix - (tmp & (0xFFFull << 52));
 #ifdef __CUDA_ARCH__
-    const double invc = __ldg(&kLogTabDev[i].invc), logc = __ldg(&kLogTabDev[i].logc);
+    const double2 e = __ldg(reinterpret_cast<const double2*>(kLogTabDev) + i); // one 16-B load
+    const double invc = e.x, logc = e.y;
 #else
     const double invc = kLogTabHost[i].invc, logc = kLogTabHost[i].logc;
 #endif
