@@ -383,6 +383,7 @@ GridImpl::~GridImpl()
     cudaFree(d_dir);
     cudaFree(d_tf);
     cudaFree(d_img);
+    cudaFree(d_sbuf);
     cudaFree(d_counters);
     cudaFree(d_scratch);
     if (ev0)

@@ -53,6 +53,8 @@ struct GridImpl {
     float4* d_tf = nullptr;
     int tf_cap = 0;
     float* d_img = nullptr;
+    float* d_sbuf = nullptr; // per-sample results of sample-chunked renders
+    size_t sbuf_cap = 0;
     size_t img_cap = 0;
     unsigned long long* d_counters = nullptr;
     double* d_scratch = nullptr;

@@ -657,6 +657,9 @@ struct DdaRegs {
 #ifndef SVDB_W_SAMPLE
 #define SVDB_W_SAMPLE 1
 #endif
+#ifndef SVDB_SAMPLE_CHUNK
+#define SVDB_SAMPLE_CHUNK 16 // max samples per work item (0: a lane owns a whole pixel)
+#endif
 #ifndef SVDB_SPEC_LOG
 #define SVDB_SPEC_LOG 1
 #endif
@@ -694,7 +697,7 @@ struct DdaRegs {
 #ifndef SVDB_ACC_DIR_COLD
 #define SVDB_ACC_DIR_COLD 0
 #endif
-template <int CODEC, int MODE>
+template <int CODEC, int MODE, bool CHUNK>
 __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
 {
     extern __shared__ float4 s_ent[];
@@ -780,7 +783,7 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
     // rows 0..6: acc0..2, tp0..2, t_ev; ratio tracking adds L0..2, Tr (pathtrace aliases those
     // names to row 6, written only by the initialisation below, before t_ev)
     __shared__ double s_cold_d[RATIO ? 11 : 7][SVDB_TRACE_THREADS];
-    __shared__ int s_cold_i[RATIO ? 7 : 6][SVDB_TRACE_THREADS];
+    __shared__ int s_cold_i[6 + (RATIO ? 1 : 0) + (CHUNK ? 1 : 0)][SVDB_TRACE_THREADS];
     const int tid = threadIdx.x;
     volatile double &acc0 = s_cold_d[0][tid], &acc1 = s_cold_d[1][tid], &acc2 = s_cold_d[2][tid];
     volatile double &tp0 = s_cold_d[3][tid], &tp1 = s_cold_d[4][tid], &tp2 = s_cold_d[5][tid];
@@ -788,7 +791,8 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
     constexpr int kR0 = RATIO ? 7 : 6, kR = RATIO ? 1 : 0;
     volatile double &L0 = s_cold_d[kR0][tid], &L1 = s_cold_d[kR0 + kR][tid], &L2 = s_cold_d[kR0 + 2 * kR][tid];
     volatile double &Tr = s_cold_d[kR0 + 3 * kR][tid];
-    volatile int& have_d = s_cold_i[RATIO ? 6 : 0][tid]; // ratio: event pending (0/1)
+    volatile int& have_d = s_cold_i[RATIO ? 6 : 0][tid];              // ratio: event pending (0/1)
+    volatile int& s_end = s_cold_i[CHUNK ? (RATIO ? 7 : 6) : 0][tid]; // chunked: end of the lane's samples
     volatile int &px = s_cold_i[0][tid], &py = s_cold_i[1][tid], &s = s_cold_i[2][tid];
     volatile int &bounces = s_cold_i[3][tid], &out_off = s_cold_i[4][tid];
     volatile float& v_ev = reinterpret_cast<volatile float&>(s_cold_i[5][tid]);
@@ -804,6 +808,8 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
     t_ev = 0.0;
     have = false;
     px = py = s = bounces = out_off = 0;
+    if constexpr (CHUNK)
+        s_end = 0;
     v_ev = 0.0f;
 #else
     int px = 0, py = 0, s = 0;
@@ -822,9 +828,16 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
 
     // path finished with float result r (render.hpp:306: accum += Vec3d(c))
     auto finish_path = [&](float r0, float r1, float r2) {
-        acc0 += double(r0);
-        acc1 += double(r1);
-        acc2 += double(r2);
+        if constexpr (CHUNK) { // the sample's result, summed in order by k_reduce
+            float* o = A.sbuf + (size_t(out_off / 3) * size_t(A.spp) + size_t(s)) * 3;
+            o[0] = r0;
+            o[1] = r1;
+            o[2] = r2;
+        } else {
+            acc0 += double(r0);
+            acc1 += double(r1);
+            acc2 += double(r2);
+        }
         ++s;
         state = kNeedPath;
     };
@@ -896,6 +909,12 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
                 goto segment;
         }
         if (state == kNeedPath) {
+            if constexpr (CHUNK) {
+                if (s == s_end) { // sample range done; k_reduce writes the pixel
+                    state = kNeedPixel;
+                    return;
+                }
+            }
             if (s == A.spp) {
 #if SVDB_COLD_SHARED
 #pragma unroll 1
@@ -1083,15 +1102,26 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             const int avail = 32 - fill;
             if (((need >> lane) & 1u) && below < avail) {
                 const int p = fill + below;
-                const long long k = unit >> 3;
-                const int w = int(unit & 7);
+                long long blk = unit;
+                int j = 0;
+                if constexpr (CHUNK) { // unit = block * nchunks + chunk (fits 32 bits)
+                    blk = (long long)(unsigned(unit) / unsigned(A.nchunks));
+                    j = int(unsigned(unit) - unsigned(blk) * unsigned(A.nchunks));
+                }
+                const long long k = blk >> 3;
+                const int w = int(blk & 7);
                 const int lx = (w & 1) * 8 + (p & 7), ly = (w >> 1) * 4 + (p >> 3);
                 const long long tt = k * A.nranks + A.rank;
                 px = int(tt % A.tiles_x) * 16 + lx;
                 py = int(tt / A.tiles_x) * 16 + ly;
                 if (px < A.cam.w && py < A.cam.h) {
                     out_off = A.packed ? (k * 256 + ly * 16 + lx) * 3 : ((long long)py * A.cam.w + px) * 3;
-                    s = 0;
+                    if constexpr (CHUNK) {
+                        s = j * A.chunk;
+                        s_end = min(A.spp, (j + 1) * A.chunk);
+                    } else {
+                        s = 0;
+                    }
                     acc0 = acc1 = acc2 = 0.0;
                     state = kNeedPath;
                 }
@@ -1210,6 +1240,45 @@ __global__ void k_unpack(const float* __restrict__ packed, int nranks, long long
         rgb[i * 3] = src[0];
         rgb[i * 3 + 1] = src[1];
         rgb[i * 3 + 2] = src[2];
+    }
+}
+
+// Sample-chunked renders: each pixel's per-sample results summed in sample order in FP64 and
+// divided by spp, exactly render_field's accumulation (render.hpp:297-310). One thread per pixel
+// slot of this rank's tiles; slots outside the image are skipped.
+__global__ void k_reduce(const float* __restrict__ sbuf, float* __restrict__ out, long long ntiles, int nranks,
+                         int rank, int tiles_x, int w, int h, int spp, int packed)
+{
+    const long long n = ntiles * 256;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long k = i >> 8;
+        const int lx = int(i & 15), ly = int((i >> 4) & 15);
+        const long long t = k * nranks + rank;
+        const int px = int(t % tiles_x) * 16 + lx, py = int(t / tiles_x) * 16 + ly;
+        if (px >= w || py >= h)
+            continue;
+        const size_t pix = packed ? size_t(k * 256 + ly * 16 + lx) : size_t(py) * size_t(w) + size_t(px);
+        const float* src = sbuf + pix * size_t(spp) * 3;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        if ((spp & 3) == 0) { // 16-B aligned rows: 4 samples (12 floats) per 3 vector loads
+            const float4* v = reinterpret_cast<const float4*>(src);
+            for (int q = 0; q < spp / 4; ++q) {
+                const float4 x = __ldg(v + 3 * q), y = __ldg(v + 3 * q + 1), z = __ldg(v + 3 * q + 2);
+                a0 += double(x.x); a1 += double(x.y); a2 += double(x.z);
+                a0 += double(x.w); a1 += double(y.x); a2 += double(y.y);
+                a0 += double(y.z); a1 += double(y.w); a2 += double(z.x);
+                a0 += double(z.y); a1 += double(z.z); a2 += double(z.w);
+            }
+        } else {
+            for (int s = 0; s < spp; ++s) {
+                a0 += double(src[3 * s]);
+                a1 += double(src[3 * s + 1]);
+                a2 += double(src[3 * s + 2]);
+            }
+        }
+        out[pix * 3] = float(a0 / double(spp));
+        out[pix * 3 + 1] = float(a1 / double(spp));
+        out[pix * 3 + 2] = float(a2 / double(spp));
     }
 }
 
@@ -1340,17 +1409,45 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     SVDB_CUDA(cudaEventRecord(e2, s));
     const bool wave = st->kernel != SVDBGPU_KERNEL_PER_PIXEL &&
                       (st->mode == SVDBGPU_MODE_PATHTRACE || st->mode == SVDBGPU_MODE_RATIO);
+    // sample-chunked work items for the path-regenerating tracers: a lane renders `chunk` samples
+    // of a pixel, not all spp, so the last items of a frame are short (the frame's tail shrinks
+    // from ~spp to ~chunk path lengths); per-sample results go through sbuf to k_reduce
+    A.sbuf = nullptr;
+    A.chunk = 0;
+    A.nchunks = 1;
+    if (wave && ntiles > 0 && !fp32) {
+        // one GPU: 16-sample items from 32 spp up (C3: 4 per pixel; fewer spp keep whole pixels,
+        // whose tail is already short); split frames (N ranks, 1/N of the work each) use 8 so
+        // the tail stays small against the shorter frame
+        const int chunk = nranks > 1 ? std::min(SVDB_SAMPLE_CHUNK / 2, std::max(4, st->spp / 2))
+                                     : (st->spp >= 32 ? SVDB_SAMPLE_CHUNK : 0);
+        const size_t npix = packed ? size_t(ntiles) * 256 : size_t(cam->width) * size_t(cam->height);
+        const size_t bytes = npix * size_t(st->spp) * 3 * sizeof(float);
+        if (chunk > 0 && chunk < st->spp && bytes <= (size_t(8) << 30)) {
+            if (bytes > g->sbuf_cap) {
+                cudaFree(g->d_sbuf);
+                g->d_sbuf = nullptr;
+                g->sbuf_cap = 0;
+                SVDB_CUDA(cudaMalloc(&g->d_sbuf, bytes));
+                g->sbuf_cap = bytes;
+            }
+            A.sbuf = g->d_sbuf;
+            A.chunk = chunk;
+            A.nchunks = (st->spp + chunk - 1) / chunk;
+        }
+    }
     if (ntiles > 0) {
         int sms = 148, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const long long n_units = ntiles * 8;
+        const long long n_units = ntiles * 8 * A.nchunks;
 #define LAUNCH_T(C, M)                                                                         \
     {                                                                                          \
         int per_sm = 1;                                                                        \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace<C, M>, SVDB_TRACE_THREADS, smem);      \
+        auto kern = A.chunk ? k_trace<C, M, true> : k_trace<C, M, false>;                         \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SVDB_TRACE_THREADS, smem);       \
         long long blocks = std::min<long long>((long long)std::max(per_sm, 1) * sms, (n_units * 32 + SVDB_TRACE_THREADS - 1) / SVDB_TRACE_THREADS); \
-        k_trace<C, M><<<unsigned(blocks), SVDB_TRACE_THREADS, smem, s>>>(A, n_units);                         \
+        kern<<<unsigned(blocks), SVDB_TRACE_THREADS, smem, s>>>(A, n_units);                          \
     }
 #define LAUNCH_R(C, M) k_render<C, M><<<unsigned(ntiles), 256, smem, s>>>(A)
 #define BY_MODE(C)                                                                             \
@@ -1374,6 +1471,11 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         }
 #undef BY_MODE
 #undef LAUNCH_R
+        if (A.chunk) {
+            const long long nslots = ntiles * 256;
+            k_reduce<<<unsigned(std::min<long long>((nslots + 255) / 256, 148LL * 64)), 256, 0, s>>>(
+                A.sbuf, d_out, ntiles, nranks, rank, A.tiles_x, cam->width, cam->height, st->spp, packed);
+        }
         cudaError_t le = cudaGetLastError();
         if (le != cudaSuccess) {
             cudaEventDestroy(e2);
@@ -1418,7 +1520,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         stats->lookups = samples * 8;
         stats->render_ms = rms;
         stats->macrocell_ms = double(range_ms) + double(mms);
-        stats->launches = (range_ms > 0.0f ? 1u : 0u) + 1u + (ntiles > 0 ? 1u : 0u);
+        stats->launches = (range_ms > 0.0f ? 1u : 0u) + 1u + (ntiles > 0 ? 1u : 0u) + (A.chunk ? 1u : 0u);
     }
     return 0;
 }

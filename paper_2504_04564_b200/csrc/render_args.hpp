@@ -38,6 +38,12 @@ struct RenderArgs {
     float* out;
     int packed;
     unsigned long long* counters;
+    // sample-chunked work (chunk > 0): a work item is (8x4 pixel block, `chunk` consecutive samples);
+    // each sample's float RGB goes to sbuf[(pixel * spp + s) * 3] and k_reduce sums a pixel's
+    // samples in index order in FP64 afterwards (render.hpp:297-310). chunk == 0: a lane owns a
+    // whole pixel and accumulates in place.
+    float* sbuf;
+    int chunk, nchunks;
 };
 
 // FP32-arithmetic tracking kernel launch (render_fast.cu): SVDBGPU_PRECISION_FP32 (all FP32) or
