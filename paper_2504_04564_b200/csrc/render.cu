@@ -1415,7 +1415,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     A.sbuf = nullptr;
     A.chunk = 0;
     A.nchunks = 1;
-    if (wave && ntiles > 0 && !fp32) {
+    if (wave && ntiles > 0) {
         // one GPU: 16-sample items from 32 spp up (C3: 4 per pixel; fewer spp keep whole pixels,
         // whose tail is already short); split frames (N ranks, 1/N of the work each) use 8 so
         // the tail stays small against the shorter frame

@@ -259,7 +259,7 @@ struct SharedDdaG {
     }
 };
 
-template <int CODEC, int MODE, typename G>
+template <int CODEC, int MODE, typename G, bool CHUNK>
 __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMixed)
     k_trace_f(const __grid_constant__ RenderArgs A, long long n_units)
 {
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
     // ratio transmittance stays FP64: a float product underflows to 0 (ending the flight) long
     // before the reference's double does, which would change the draws that follow
     __shared__ double s_tr[RATIO ? kT : 1];
-    __shared__ int s_ci[RATIO ? 6 : 5][kT];            // px, py, s, bounces, out_off (+ have)
+    __shared__ int s_ci[5 + (RATIO ? 1 : 0) + (CHUNK ? 1 : 0)][kT]; // px, py, s, bounces, out_off (+ have, s_end)
     volatile float* cold = &s_cold[0][tid];
     volatile int* ci = &s_ci[0][tid];
     volatile double* sum = &s_sum[0][tid];
@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
     volatile double& Tr = reinterpret_cast<volatile double*>(s_tr)[RATIO ? tid : 0]; // ratio only
     volatile int &px = ci[0], &py = ci[kT], &s = ci[2 * kT], &bounces = ci[3 * kT], &out_off = ci[4 * kT];
     volatile int& have = ci[(RATIO ? 5 : 0) * kT]; // ratio only
+    volatile int& s_end = ci[(CHUNK ? (RATIO ? 6 : 5) : 0) * kT]; // chunked: end of the lane's samples
 
     Accessor<CODEC> acc(A.g);
     auto acc_io = [&](bool store) {
@@ -354,9 +355,16 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
     int fill = 32;
 
     auto finish_path = [&](float r0, float r1, float r2) {
-        sum[0] += double(r0);
-        sum[kT] += double(r1);
-        sum[2 * kT] += double(r2);
+        if constexpr (CHUNK) { // the sample's result, summed in order by k_reduce (render.cu)
+            float* o = A.sbuf + (size_t(out_off / 3) * size_t(A.spp) + size_t(s)) * 3;
+            o[0] = r0;
+            o[1] = r1;
+            o[2] = r2;
+        } else {
+            sum[0] += double(r0);
+            sum[kT] += double(r1);
+            sum[2 * kT] += double(r2);
+        }
         s = s + 1;
         state = kNeedPath;
     };
@@ -441,6 +449,12 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
                 goto segment;
         }
         if (state == kNeedPath) {
+            if constexpr (CHUNK) {
+                if (s == s_end) {
+                    state = kNeedPixel;
+                    return;
+                }
+            }
             if (s == A.spp) {
                 const double inv_spp = 1.0 / double(A.spp);
                 A.out[out_off] = float(sum[0] * inv_spp);
@@ -570,8 +584,14 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
             const int avail = 32 - fill;
             if (((need >> lane) & 1u) && below < avail) {
                 const int p = fill + below;
-                const long long k = unit >> 3;
-                const int w = int(unit & 7);
+                long long blk = unit;
+                int j = 0;
+                if constexpr (CHUNK) { // unit = block * nchunks + chunk (fits 32 bits)
+                    blk = (long long)(unsigned(unit) / unsigned(A.nchunks));
+                    j = int(unsigned(unit) - unsigned(blk) * unsigned(A.nchunks));
+                }
+                const long long k = blk >> 3;
+                const int w = int(blk & 7);
                 const int lx = (w & 1) * 8 + (p & 7), ly = (w >> 1) * 4 + (p >> 3);
                 const long long tt = k * A.nranks + A.rank;
                 const int qx = int(tt % A.tiles_x) * 16 + lx, qy = int(tt / A.tiles_x) * 16 + ly;
@@ -579,8 +599,13 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
                     px = qx;
                     py = qy;
                     out_off = int(A.packed ? (k * 256 + ly * 16 + lx) * 3 : ((long long)qy * A.cam.w + qx) * 3);
-                    s = 0;
-                    sum[0] = sum[kT] = sum[2 * kT] = 0.0;
+                    if constexpr (CHUNK) {
+                        s = j * A.chunk;
+                        s_end = min(A.spp, (j + 1) * A.chunk);
+                    } else {
+                        s = 0;
+                        sum[0] = sum[kT] = sum[2 * kT] = 0.0;
+                    }
                     state = kNeedPath;
                 }
             }
@@ -623,9 +648,10 @@ int launch(const RenderArgs& A, long long n_units, size_t smem, cudaStream_t s)
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace_f<CODEC, MODE, G>, kT, smem);
+    auto kern = A.chunk ? k_trace_f<CODEC, MODE, G, true> : k_trace_f<CODEC, MODE, G, false>;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kT, smem);
     const long long blocks = std::min<long long>((long long)std::max(per_sm, 1) * sms, (n_units * 32 + kT - 1) / kT);
-    k_trace_f<CODEC, MODE, G><<<unsigned(blocks), kT, smem, s>>>(A, n_units);
+    kern<<<unsigned(blocks), kT, smem, s>>>(A, n_units);
     return 0;
 }
 
