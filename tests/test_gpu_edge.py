@@ -127,3 +127,47 @@ def test_node_walk_without_leaf_directory_is_identical(gpu, ref, monkeypatch):
         a = P.render(with_dir, TF, cam, st).pixels
         b = P.render(no_dir, TF, cam, st).pixels
         assert np.array_equal(bits(a), bits(b))
+
+
+@pytest.mark.parametrize("spp,nranks", [(40, 1), (33, 1), (36, 3), (17, 2)])
+def test_sample_chunked_items_match_reference(gpu, ref, spp, nranks):
+    # sample-chunked work items (>= 32 spp on one GPU, any split frame): per-sample results are
+    # summed in order afterwards, so frames stay bit-identical, for chunk counts that do not divide
+    # spp and for spp not a multiple of 4 (scalar reduce path), on full and packed tile splits
+    svdb = _tile_grid(ref, dims=(48, 40, 36), background=0.2, seed=19)
+    g = P.DeviceGrid(svdb, P.Codec.f32)
+    cam = P.Camera(position=(23.5, 70.0, -60.0), look_at=(23.5, 19.5, 17.5), width=37, height=29)
+    st = P.RenderSettings(spp=spp, seed=77, max_bounces=16, rr_start_bounce=2)
+    want = ref.open(svdb).render(TF, cam, st)
+    full = np.zeros_like(want)
+    tiles_x = (cam.width + 15) // 16
+    for r in range(nranks):
+        img = P.render(g, TF, cam, st, tile_rank=r, tile_nranks=nranks).pixels
+        for t in range(r, tiles_x * ((cam.height + 15) // 16), nranks):
+            y0, x0 = (t // tiles_x) * 16, (t % tiles_x) * 16
+            full[y0:y0 + 16, x0:x0 + 16] = img[y0:y0 + 16, x0:x0 + 16]
+    _check(full, want, min_same=0.98)
+
+
+@pytest.mark.parametrize("spp", [4, 36])
+def test_packed_device_split_and_unpack_match_reference(gpu, ref, spp):
+    # the multi-GPU data path on one GPU: each "rank" renders its tiles into a packed device buffer
+    # (svdbgpu_render_device, packed=1; sample-chunked at 36 spp), the buffers are concatenated as the
+    # NCCL gather would and k_unpack assembles the frame -> the reference's frame bit for bit
+    torch = pytest.importorskip("torch")
+    svdb = _tile_grid(ref, dims=(48, 40, 36), background=0.2, seed=23)
+    g = P.DeviceGrid(svdb, P.Codec.f32)
+    cam = P.Camera(position=(23.5, 70.0, -60.0), look_at=(23.5, 19.5, 17.5), width=53, height=35)
+    st = P.RenderSettings(spp=spp, seed=5, max_bounces=8, rr_start_bounce=2)
+    want = ref.open(svdb).render(TF, cam, st)
+    nranks = 3
+    max_tiles = P.tiles_for_rank(cam.width, cam.height, 0, nranks)
+    bufs = [torch.zeros(max_tiles * 768, dtype=torch.float32, device="cuda") for _ in range(nranks)]
+    for r in range(nranks):
+        P.render_device(g, TF, cam, st, bufs[r].data_ptr(), 0, packed=True, tile_rank=r, tile_nranks=nranks)
+    allp = torch.cat(bufs)
+    frame = torch.zeros(cam.height * cam.width * 3, dtype=torch.float32, device="cuda")
+    P.unpack_tiles_device(allp.data_ptr(), nranks, max_tiles, cam.width, cam.height, frame.data_ptr(), 0)
+    torch.cuda.synchronize()
+    got = frame.cpu().numpy().reshape(cam.height, cam.width, 3)
+    _check(got, want, min_same=0.98)
