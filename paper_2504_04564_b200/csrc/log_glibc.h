@@ -85,8 +85,12 @@ SVDB_HD double glibc_log(double x)
     const int k = int(static_cast<int64_t>(tmp) >> 52);
     const uint64_t iz = ix - (tmp & (0xFFFull << 52));
 #ifdef __CUDA_ARCH__
-    const double2 e = __ldg(reinterpret_cast<const double2*>(kLogTabDev) + i); // one 16-B load
-    const double invc = e.x, logc = e.y;
+    // one 16-B load; the 2 KB table is marked evict-last so the leaf data streaming through L1
+    // does not push it out
+    double invc, logc;
+    asm("ld.global.nc.L1::evict_last.v2.f64 {%0, %1}, [%2];"
+        : "=d"(invc), "=d"(logc)
+        : "l"(reinterpret_cast<const double2*>(kLogTabDev) + i));
 #else
     const double invc = kLogTabHost[i].invc, logc = kLogTabHost[i].logc;
 #endif
