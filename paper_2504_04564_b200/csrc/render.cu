@@ -657,6 +657,9 @@ struct DdaRegs {
 #ifndef SVDB_W_SAMPLE
 #define SVDB_W_SAMPLE 1
 #endif
+#ifndef SVDB_SPLIT_CHUNK
+#define SVDB_SPLIT_CHUNK 4 // max samples per work item when the frame is split over ranks
+#endif
 #ifndef SVDB_SAMPLE_CHUNK
 #define SVDB_SAMPLE_CHUNK 16 // max samples per work item (0: a lane owns a whole pixel)
 #endif
@@ -1417,9 +1420,9 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     A.nchunks = 1;
     if (wave && ntiles > 0) {
         // one GPU: 16-sample items from 32 spp up (C3: 4 per pixel; fewer spp keep whole pixels,
-        // whose tail is already short); split frames (N ranks, 1/N of the work each) use 8 so
+        // whose tail is already short); split frames (N ranks, 1/N of the work each) use 4 so
         // the tail stays small against the shorter frame
-        const int chunk = nranks > 1 ? std::min(SVDB_SAMPLE_CHUNK / 2, std::max(4, st->spp / 2))
+        const int chunk = nranks > 1 ? std::min(SVDB_SPLIT_CHUNK, std::max(1, st->spp / 2))
                                      : (st->spp >= 32 ? SVDB_SAMPLE_CHUNK : 0);
         const size_t npix = packed ? size_t(ntiles) * 256 : size_t(cam->width) * size_t(cam->height);
         const size_t bytes = npix * size_t(st->spp) * 3 * sizeof(float);

@@ -18,6 +18,7 @@ del vol
 g = P.DeviceGrid(svdb, sc.codec)
 cam = sc.camera()
 P.render(g, sc.tf, cam, sc.settings)  # warm-up (majorants, caches)
+P.render(g, sc.tf, cam, sc.settings, tile_rank=0, tile_nranks=2)  # warm-up of the split path's buffers
 full = P.render(g, sc.tf, cam, sc.settings).stats["render_ms"]
 out = {"config": name, "full_frame_ms": full, "splits": {}}
 for n in (2, 4, 8):
