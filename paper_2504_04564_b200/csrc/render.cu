@@ -657,6 +657,9 @@ struct DdaRegs {
 #ifndef SVDB_W_SAMPLE
 #define SVDB_W_SAMPLE 1
 #endif
+#ifndef SVDB_CHUNK_MIN_SPP
+#define SVDB_CHUNK_MIN_SPP 16 // one GPU: whole-pixel items below this many samples per pixel
+#endif
 #ifndef SVDB_SPLIT_CHUNK
 #define SVDB_SPLIT_CHUNK 4 // max samples per work item when the frame is split over ranks
 #endif
@@ -1419,11 +1422,11 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     A.chunk = 0;
     A.nchunks = 1;
     if (wave && ntiles > 0) {
-        // one GPU: 16-sample items from 32 spp up (C3: 4 per pixel; fewer spp keep whole pixels,
-        // whose tail is already short); split frames (N ranks, 1/N of the work each) use 4 so
-        // the tail stays small against the shorter frame
+        // one GPU: items of up to 16 samples, at least 2 per pixel, from 16 spp up (C3: 4 per pixel,
+        // C2 / C4: 2); fewer spp keep whole pixels, whose tail is already short. Split frames
+        // (N ranks, 1/N of the work each) use 4 so the tail stays small against the shorter frame
         const int chunk = nranks > 1 ? std::min(SVDB_SPLIT_CHUNK, std::max(1, st->spp / 2))
-                                     : (st->spp >= 32 ? SVDB_SAMPLE_CHUNK : 0);
+                                     : (st->spp >= SVDB_CHUNK_MIN_SPP ? std::min(SVDB_SAMPLE_CHUNK, st->spp / 2) : 0);
         const size_t npix = packed ? size_t(ntiles) * 256 : size_t(cam->width) * size_t(cam->height);
         const size_t bytes = npix * size_t(st->spp) * 3 * sizeof(float);
         if (chunk > 0 && chunk < st->spp && bytes <= (size_t(8) << 30)) {
