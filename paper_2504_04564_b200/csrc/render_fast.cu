@@ -41,6 +41,9 @@ constexpr int kT = 64;          // threads per CTA
 #ifndef SVDB_F_PERSIST_ACC
 #define SVDB_F_PERSIST_ACC 0 // accessor caches kept between gathers (off: cold locate = one directory load)
 #endif
+#ifndef SVDB_F_REBASE
+#define SVDB_F_REBASE 0 // FP32: camera ray built and clipped in FP64, origin moved to the volume entry (measured: DESIGN.md §3.4)
+#endif
 #ifndef SVDB_F_ADV_ITERS
 #define SVDB_F_ADV_ITERS 3
 #endif
@@ -172,6 +175,41 @@ __device__ __forceinline__ RayG<G> camera_ray_g(const CamArgs& c, G px, G py)
     for (int a = 0; a < 3; ++a)
         r.d[a] = d[a] / len;
     return r;
+}
+
+// FP32 geometry: the camera ray in FP64 (53-bit jitter), clipped to [0, hi] (dda.hpp:25-46) and
+// restarted at the entry point, so the float distances t along the first segment start near 0
+// instead of at the camera distance (C4: ~2,000-4,000 voxels, where a float t is off by ~2e-4)
+__device__ __forceinline__ RayG<float> camera_ray_entry(const CamArgs& c, double px, double py, const double hi[3])
+{
+    const RayG<double> r = camera_ray_g<double>(c, px, py);
+    double t0 = 0.0, t1 = __longlong_as_double(0x7ff0000000000000ll);
+    bool hit = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (r.d[a] == 0.0) {
+            hit = hit && !(r.o[a] < 0.0 || r.o[a] > hi[a]);
+            continue;
+        }
+        const double inv = 1.0 / r.d[a];
+        double ta = (0.0 - r.o[a]) * inv, tb = (hi[a] - r.o[a]) * inv;
+        if (ta > tb) {
+            const double tt = ta;
+            ta = tb;
+            tb = tt;
+        }
+        t0 = fmax(t0, ta);
+        t1 = fmin(t1, tb);
+    }
+    if (!(hit && t0 <= t1))
+        t0 = 0.0; // a miss stays a miss from the camera
+    RayG<float> f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        f.o[a] = float(r.o[a] + r.d[a] * t0);
+        f.d[a] = float(r.d[a]);
+    }
+    return f;
 }
 
 // Macrocell DDA (dda.hpp:25-109) in float, per-lane state in shared memory (SoA)
@@ -468,14 +506,20 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
                 rng.state = r0.state;
             }
             G jx, jy;
-            if constexpr (MIXED) {
+            if constexpr (!MIXED && SVDB_F_REBASE) {
+                const double djx = rng.uniform53(), djy = rng.uniform53();
+                const double dhi[3] = {A.hi[0], A.hi[1], A.hi[2]};
+                ray_store(camera_ray_entry(A.cam, double(px) + djx, double(py) + djy, dhi));
+                jx = jy = G(0);
+            } else if constexpr (MIXED) {
                 jx = rng.uniform53();
                 jy = rng.uniform53();
             } else {
                 jx = rng.uniform();
                 jy = rng.uniform();
             }
-            ray_store(camera_ray_g<G>(A.cam, G(px) + jx, G(py) + jy));
+            if constexpr (MIXED || !SVDB_F_REBASE)
+                ray_store(camera_ray_g<G>(A.cam, G(px) + jx, G(py) + jy));
             tp(0) = tp(1) = tp(2) = 1.0f;
             bounces = 0;
             if constexpr (RATIO)
