@@ -688,6 +688,9 @@ struct DdaRegs {
 #ifndef SVDB_COLD_SHARED
 #define SVDB_COLD_SHARED 1
 #endif
+#ifndef SVDB_SPEC_LOG_GATE
+#define SVDB_SPEC_LOG_GATE 0 // 1: skip the speculative log when the next cell is known empty (measured slower)
+#endif
 #ifndef SVDB_MAJ_AHEAD
 #define SVDB_MAJ_AHEAD 1
 #endif
@@ -972,7 +975,13 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
         // the step draw's log does not depend on the DDA: compute it from the next uniform before
         // the cell lookup (independent FP64 chains interleave); the draw is consumed only if the
         // cell has draws, so the stream is unchanged
+#if SVDB_SPEC_LOG_GATE && SVDB_MAJ_AHEAD
+        // a lane about to enter a cell whose majorant (loaded one visit ahead) is 0 draws nothing
+        // there: skip its log, so warps whose advancing lanes all cross empty cells skip it
+        const double lg = (state == kInCell || inv_ahead > 0.0) ? step_log(1.0 - rng.peek()) : 0.0;
+#else
         const double lg = step_log(1.0 - rng.peek());
+#endif
 #endif
         if (state == kNeedCell) {
             int c[3];
