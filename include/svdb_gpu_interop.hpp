@@ -15,8 +15,12 @@
 // GridCache for repeated frames.
 #pragma once
 
+#include <cstdlib>
+#include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
+#include <tuple>
 
 #include "svdb_gpu.hpp"
 
@@ -78,35 +82,129 @@ inline Grid upload(const svdb::FrozenGrid& g, Codec codec = Codec::f32, int devi
     throw svdb::Error(svdb::Errc::io_error, "unreachable");
 }
 
-/// Per-process cache: one device grid per FrozenGrid (frames re-render the same grid). Entries are
-/// keyed by address and codec and validated by a fingerprint of the grid's shape and storage
-/// (dims, background, node counts, vector data pointers, first/last leaf values), so a different
-/// grid later constructed at the same address is re-uploaded instead of served stale. FrozenGrid
-/// is immutable by contract (frozen.hpp:225-227); in-place edits of leaf values are not detected.
+/// Per-process cache of device grids, one per (FrozenGrid, codec, device): frames re-render the
+/// same grid, so the upload is paid once. Entries are keyed by address and validated by a
+/// fingerprint of the grid's shape and storage (dims, background, node counts, vector data
+/// pointers, first/last leaf values), so a different grid later constructed at the same address is
+/// re-uploaded instead of served stale. FrozenGrid is immutable by contract (frozen.hpp:225-227);
+/// in-place edits of leaf values are not detected.
+///
+/// The cache is bounded: when the resident device bytes exceed budget() (default 16 GiB, or
+/// SVDBGPU_CACHE_BYTES) the least recently used entries are evicted. get() hands out shared
+/// ownership, so an in-flight render keeps its grid alive even if another thread evicts it.
+/// evict(grid) drops one grid's entries (call it before destroying a FrozenGrid you will not render
+/// again); clear() drops everything.
 class GridCache {
 public:
-    static Grid& get(const svdb::FrozenGrid& g, Codec codec)
+    static std::shared_ptr<Grid> get(const svdb::FrozenGrid& g, Codec codec, int device = 0)
     {
-        struct Entry {
-            std::vector<uint64_t> fp;
-            std::unique_ptr<Grid> grid;
-        };
-        static std::mutex mu;
-        static std::map<std::pair<const svdb::FrozenGrid*, int>, Entry> cache;
-        std::lock_guard<std::mutex> lk(mu);
+        State& st = state();
         std::vector<uint64_t> fp = fingerprint(g);
-        auto key = std::make_pair(&g, int(codec));
-        auto it = cache.find(key);
-        if (it != cache.end() && it->second.fp != fp) {
-            cache.erase(it);
-            it = cache.end();
+        const Key key{&g, int(codec), device};
+        {
+            std::lock_guard<std::mutex> lk(st.mu);
+            auto it = st.map.find(key);
+            if (it != st.map.end()) {
+                if (it->second.fp == fp) {
+                    it->second.tick = ++st.clock;
+                    return it->second.grid;
+                }
+                st.bytes -= it->second.bytes;
+                st.map.erase(it);
+            }
         }
-        if (it == cache.end())
-            it = cache.emplace(key, Entry{fp, std::make_unique<Grid>(upload(g, codec))}).first;
-        return *it->second.grid;
+        // upload outside the lock (seconds for GB-sized grids); a racing upload of the same key
+        // keeps the first one inserted
+        auto grid = std::make_shared<Grid>(upload(g, codec, device));
+        const uint64_t bytes = grid->info().device_bytes;
+        std::lock_guard<std::mutex> lk(st.mu);
+        auto it = st.map.find(key);
+        if (it != st.map.end() && it->second.fp == fp) {
+            it->second.tick = ++st.clock;
+            return it->second.grid;
+        }
+        if (it != st.map.end()) {
+            st.bytes -= it->second.bytes;
+            st.map.erase(it);
+        }
+        st.map[key] = Entry{fp, grid, bytes, ++st.clock};
+        st.bytes += bytes;
+        while (st.bytes > st.budget && st.map.size() > 1) { // never evict the entry just inserted
+            auto lru = st.map.end();
+            for (auto e = st.map.begin(); e != st.map.end(); ++e)
+                if (!(e->first == key) && (lru == st.map.end() || e->second.tick < lru->second.tick))
+                    lru = e;
+            st.bytes -= lru->second.bytes;
+            st.map.erase(lru);
+        }
+        return grid;
+    }
+
+    /// Drop every cached device grid of `g` (all codecs and devices).
+    static void evict(const svdb::FrozenGrid& g)
+    {
+        State& st = state();
+        std::lock_guard<std::mutex> lk(st.mu);
+        for (auto it = st.map.begin(); it != st.map.end();) {
+            if (std::get<0>(it->first) == &g) {
+                st.bytes -= it->second.bytes;
+                it = st.map.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+    static void clear()
+    {
+        State& st = state();
+        std::lock_guard<std::mutex> lk(st.mu);
+        st.map.clear();
+        st.bytes = 0;
+    }
+    static void set_budget(uint64_t bytes)
+    {
+        State& st = state();
+        std::lock_guard<std::mutex> lk(st.mu);
+        st.budget = bytes;
+    }
+    static uint64_t budget() { return state().budget; }
+    static uint64_t resident_bytes()
+    {
+        State& st = state();
+        std::lock_guard<std::mutex> lk(st.mu);
+        return st.bytes;
+    }
+    static size_t size()
+    {
+        State& st = state();
+        std::lock_guard<std::mutex> lk(st.mu);
+        return st.map.size();
     }
 
 private:
+    using Key = std::tuple<const svdb::FrozenGrid*, int, int>;
+    struct Entry {
+        std::vector<uint64_t> fp;
+        std::shared_ptr<Grid> grid;
+        uint64_t bytes = 0, tick = 0;
+    };
+    struct State {
+        std::mutex mu;
+        std::map<Key, Entry> map;
+        uint64_t bytes = 0, clock = 0;
+        uint64_t budget = default_budget();
+    };
+    static State& state()
+    {
+        static State s;
+        return s;
+    }
+    static uint64_t default_budget()
+    {
+        if (const char* e = std::getenv("SVDBGPU_CACHE_BYTES"))
+            return std::strtoull(e, nullptr, 10);
+        return uint64_t(16) << 30;
+    }
     static std::vector<uint64_t> fingerprint(const svdb::FrozenGrid& g)
     {
         auto bits = [](float f) {
@@ -133,8 +231,8 @@ inline svdb::Image render(const svdb::FrozenGrid& grid, const svdb::TransferFunc
                           const svdb::RenderSettings& settings, Codec codec = Codec::f32)
 {
     try {
-        Grid& g = GridCache::get(grid, codec);
-        Image img = render(g, convert(tf), convert(cam), convert(settings));
+        std::shared_ptr<Grid> g = GridCache::get(grid, codec);
+        Image img = render(*g, convert(tf), convert(cam), convert(settings));
         svdb::Image out;
         out.width = img.width;
         out.height = img.height;
@@ -152,8 +250,8 @@ inline svdb::Image render(const svdb::FrozenGrid& grid, const svdb::TransferFunc
 inline float sample(const svdb::FrozenGrid& grid, const svdb::Vec3d& p, svdb::SampleMode mode)
 {
     try {
-        Grid& g = GridCache::get(grid, Codec::f32);
-        return sample(g, Vec3d{p.x, p.y, p.z}, mode == svdb::SampleMode::nearest ? SampleMode::nearest
+        std::shared_ptr<Grid> g = GridCache::get(grid, Codec::f32);
+        return sample(*g, Vec3d{p.x, p.y, p.z}, mode == svdb::SampleMode::nearest ? SampleMode::nearest
                                                                                  : SampleMode::trilinear);
     } catch (const Error& e) {
         rethrow_as_svdb(e);

@@ -293,10 +293,13 @@ int svdbgpu_render(svdbgpu_grid* g, const svdbgpu_tf* tf, const svdbgpu_camera* 
         if (cam->width < 1 || cam->height < 1)
             return fail(Errc::size_mismatch, "image size must be positive");
         const int nranks = s->tile_nranks > 0 ? s->tile_nranks : 1;
+        if (nranks > 1 && (s->tile_rank < 0 || s->tile_rank >= nranks))
+            return fail_code(SVDBGPU_E_INVALID_ARG, "tile_rank out of range");
         const size_t pix = size_t(cam->width) * size_t(cam->height);
+        // a rank may own no tiles (small image, many ranks): it renders nothing and succeeds
         const size_t need = (nranks > 1 ? size_t(tiles_for_rank(cam->width, cam->height, s->tile_rank, nranks)) * 256
                                         : pix) * 3 * sizeof(float);
-        if (need > G->img_cap) {
+        if (need > G->img_cap || !G->d_img) {
             cudaFree(G->d_img);
             G->d_img = nullptr;
             G->img_cap = 0;

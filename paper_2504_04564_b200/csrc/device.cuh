@@ -77,9 +77,6 @@ __device__ __forceinline__ int find_upper(const DevGrid& g, int ox, int oy, int 
 
 // Per-thread read-through cache (Accessor, frozen.hpp:228-277). Keys are the coordinate-derived
 // node origins; values never depend on the cache state (test_tree.cpp:247-271).
-#ifndef SVDB_LEAF_DIR
-#define SVDB_LEAF_DIR 1
-#endif
 template <int CODEC>
 struct Accessor {
     const DevGrid* g;
@@ -170,7 +167,6 @@ struct Accessor {
     {
         if (in_leaf(x, y, z))
             return true;
-#if SVDB_LEAF_DIR
         if (g->dir) {
             const unsigned cx = unsigned(x) >> 3, cy = unsigned(y) >> 3, cz = unsigned(z) >> 3;
             if (x >= 0 && y >= 0 && z >= 0 && cx < unsigned(g->dir_dims[0]) && cy < unsigned(g->dir_dims[1]) &&
@@ -189,7 +185,6 @@ struct Accessor {
                 return true;
             }
         }
-#endif
         if (!in_lower(x, y, z)) {
             const int ox = x & ~4095, oy = y & ~4095, oz = z & ~4095;
             if (!(ox == ux && oy == uy && oz == uz)) {
@@ -270,33 +265,14 @@ __device__ __forceinline__ float trilerp(const double v[8], double wx, double wy
     return float(v0 * (1.0 - wz) + v1 * wz);
 }
 
-// Apron offset of extended-brick voxel (x,y,z) in [0,8]^3 with at least one coordinate == 8
-// (region r = bits of the axes at 8; see k_build_apron in grid.cu)
-__device__ __forceinline__ int apron_offset(int r, int x, int y, int z)
-{
-    switch (r) {
-    case 1: return y + 8 * z;
-    case 2: return 64 + x + 8 * z;
-    case 4: return 128 + x + 8 * y;
-    case 3: return 192 + z;
-    case 5: return 200 + y;
-    case 6: return 208 + x;
-    default: return 216;
-    }
-}
-
 // One tap of the 9^3 stencil brick of the cached leaf: own block or apron, decoded with the
 // owning block's parameters. All eight taps of a sample are independent loads.
-#ifndef SVDB_BRANCHLESS_TAP
-#define SVDB_BRANCHLESS_TAP 1
-#endif
 template <int CODEC>
 __device__ __forceinline__ float brick_tap_f(const Accessor<CODEC>& a, int x, int y, int z)
 {
     const uint8_t* base = a.g->codes + size_t(a.leaf) * a.g->leaf_stride;
     const int r = (x >> 3) | ((y >> 3) << 1) | ((z >> 3) << 2);
-#if SVDB_BRANCHLESS_TAP
-    // Same element as the region switch below, from per-region coefficient tables, so lanes whose
+    // The element of the own block / apron region, from per-region coefficient tables, so lanes whose
     // taps fall in different regions do not diverge: own block (r = 0) x + 8y + 64z; apron region
     // r packs its remaining axes x-fastest with stride 8 after the 512 own elements.
     const int xr = x & 7, yr = y & 7, zr = z & 7;
@@ -325,17 +301,6 @@ __device__ __forceinline__ float brick_tap_f(const Accessor<CODEC>& a, int x, in
             return decode_code<CODEC>(__ldg(base + e), lo, sc);
         }
     }
-#else
-    if (r == 0)
-        return decode<CODEC>(*a.g, a.leaf, x + 8 * (y + 8 * z), a.lo, a.sc);
-    const int e = apron_offset(r, x & 7, y & 7, z & 7);
-    if constexpr (CODEC == kCodecF32) {
-        return __ldg(reinterpret_cast<const float*>(base + a.g->main_bytes) + e);
-    } else {
-        const float2 p = __ldg(a.g->lparams + size_t(a.leaf) * 8 + r);
-        return decode_code<CODEC>(__ldg(base + a.g->main_bytes + e), p.x, p.y);
-    }
-#endif
 }
 
 template <int CODEC>

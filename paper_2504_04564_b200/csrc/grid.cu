@@ -331,10 +331,15 @@ __global__ void k_majorants(DevTF tf, const float4* __restrict__ ent_g, const fl
                             double* __restrict__ inv_maj, float* __restrict__ inv_maj_f,
                             uint8_t* __restrict__ empty)
 {
-    extern __shared__ float4 ent[];
-    for (int i = threadIdx.x; i < tf.n; i += blockDim.x)
-        ent[i] = ent_g[i];
-    __syncthreads();
+    extern __shared__ float4 s_tf[];
+    const float4* ent = s_tf;
+    if (tf.n > kTfSmemMax) {
+        ent = ent_g;
+    } else {
+        for (int i = threadIdx.x; i < tf.n; i += blockDim.x)
+            s_tf[i] = ent_g[i];
+        __syncthreads();
+    }
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n)
         return;
@@ -488,7 +493,7 @@ int GridImpl::ensure_ranges(cudaStream_t s, float* ms, int cd)
 int majorants(GridImpl* g, const DevTF& tf, cudaStream_t s, uint8_t* d_empty)
 {
     int nc = g->cells[0] * g->cells[1] * g->cells[2];
-    k_majorants<<<(nc + 255) / 256, 256, sizeof(float4) * size_t(tf.n), s>>>(tf, g->d_tf, g->d_cmin, g->d_cmax, nc,
+    k_majorants<<<(nc + 255) / 256, 256, tf_smem_bytes(tf.n), s>>>(tf, g->d_tf, g->d_cmin, g->d_cmax, nc,
                                                                             g->d_maj, g->d_inv_maj, g->d_inv_maj_f, d_empty);
     SVDB_CUDA(cudaGetLastError());
     return 0;

@@ -40,6 +40,11 @@ struct DevTF {
     double inv_range;
 };
 
+// Transfer-function entries are staged in shared memory up to this many (16 KB); larger tables are
+// read from global memory (L1-cached) so any entry count the reference accepts renders.
+constexpr int kTfSmemMax = 1024;
+__host__ __device__ inline size_t tf_smem_bytes(int n) { return n <= kTfSmemMax ? size_t(n) * 16 : 0; }
+
 constexpr int kCodecF32 = 0, kCodecUnorm8 = 1, kCodecAffine8 = 2, kCodecAffine4 = 3;
 
 } // namespace svdbgpu

@@ -29,6 +29,17 @@ namespace svdbgpu {
 
 namespace {
 
+// TF entries to shared memory when they fit (kTfSmemMax), else read in place from global memory
+__device__ __forceinline__ const float4* stage_tf(const RenderArgs& A, float4* smem)
+{
+    if (A.tf.n > kTfSmemMax)
+        return A.tf_ent;
+    for (int i = threadIdx.x; i < A.tf.n; i += blockDim.x)
+        smem[i] = A.tf_ent[i];
+    __syncthreads();
+    return smem;
+}
+
 constexpr double kPi = 3.14159265358979323846;
 
 __device__ __forceinline__ double kInf() { return __longlong_as_double(0x7ff0000000000000ll); }
@@ -390,10 +401,8 @@ __device__ __forceinline__ Ray camera_ray(const CamArgs& c, double px, double py
 template <int CODEC, int MODE>
 __global__ void __launch_bounds__(256) k_render(const __grid_constant__ RenderArgs A)
 {
-    extern __shared__ float4 s_ent[];
-    for (int i = threadIdx.x; i < A.tf.n; i += blockDim.x)
-        s_ent[i] = A.tf_ent[i];
-    __syncthreads();
+    extern __shared__ float4 s_tf[];
+    const float4* s_ent = stage_tf(A, s_tf);
 
     const long long k = blockIdx.x; // k-th tile of this rank
     const long long t = k * A.nranks + A.rank;
@@ -562,244 +571,67 @@ struct SharedDda {
     }
 };
 
-// The moving part of a SharedDda (cell, t_next, t_cur, t1, done) held in registers across one
-// advance phase; step and t_delta are read from shared memory only for the axis that steps.
-// next() is SharedDda::next's arithmetic exactly.
-template <int T>
-struct DdaRegs {
-    SharedDda<T>* s;
-    int c[3];
-    double n[3], t_cur, t1;
-    bool dn;
-    __device__ __forceinline__ void load(SharedDda<T>& d)
-    {
-        s = &d;
-        c[0] = d.ci(0);
-        c[1] = d.ci(1);
-        c[2] = d.ci(2);
-        n[0] = d.cd(0);
-        n[1] = d.cd(1);
-        n[2] = d.cd(2);
-        t_cur = d.cd(6);
-        t1 = d.cd(7);
-        dn = d.done();
-    }
-    __device__ __forceinline__ void store()
-    {
-        s->ci(0) = c[0];
-        s->ci(1) = c[1];
-        s->ci(2) = c[2];
-        s->cd(0) = n[0];
-        s->cd(1) = n[1];
-        s->cd(2) = n[2];
-        s->cd(6) = t_cur;
-        s->ci(6) = dn ? 1 : 0;
-    }
-    __device__ __forceinline__ bool done() const { return dn; }
-    __device__ __forceinline__ int index(const int cells[3]) const { return c[0] + cells[0] * (c[1] + cells[1] * c[2]); }
-    __device__ __forceinline__ bool next(const int cells[3], int cell[3], double& ta, double& tb)
-    {
-        if (dn)
-            return false;
-        const bool ax1 = n[1] < n[0];
-        const double tm = ax1 ? n[1] : n[0];
-        const bool ax2 = n[2] < tm;
-        const int axis = ax2 ? 2 : (ax1 ? 1 : 0);
-        double t_exit = dmin(ax2 ? n[2] : tm, t1);
-        t_exit = dmax(t_exit, t_cur);
-        cell[0] = c[0];
-        cell[1] = c[1];
-        cell[2] = c[2];
-        ta = t_cur;
-        tb = t_exit;
-        if (t_exit >= t1) {
-            dn = true;
-            return true;
-        }
-        t_cur = t_exit;
-        const int cn = (axis == 0 ? c[0] : (axis == 1 ? c[1] : c[2])) + s->stepv(axis);
-        if (axis == 0)
-            c[0] = cn;
-        else if (axis == 1)
-            c[1] = cn;
-        else
-            c[2] = cn;
-        if (cn < 0 || cn >= cells[axis]) {
-            dn = true;
-        } else {
-            const double nn = (axis == 0 ? n[0] : (axis == 1 ? n[1] : n[2])) + s->cd(3 + axis);
-            if (axis == 0)
-                n[0] = nn;
-            else if (axis == 1)
-                n[1] = nn;
-            else
-                n[2] = nn;
-        }
-        return true;
-    }
-};
+constexpr int kTraceThreads = 64;   // 2 warps per CTA
+constexpr int kTraceMinBlocks = 14; // <= 72 registers, 14.3 KB shared: 28 resident warps per SM
+constexpr int kAdvIters = 3;        // advance steps per advance-phase invocation
+constexpr int kChunkMinSpp = 16;    // one GPU: whole-pixel work items below this many samples per pixel
+constexpr int kSplitChunk = 4;      // max samples per work item when the frame is split over ranks
+constexpr int kSampleChunk = 16;    // max samples per work item on one GPU
 
-#ifndef SVDB_DDA_REGS
-#define SVDB_DDA_REGS 0
-#endif
-#ifndef SVDB_TRACE_THREADS
-#define SVDB_TRACE_THREADS 64 // 2 warps per CTA, <= 80 registers: 24 resident warps per SM
-#endif
-#ifndef SVDB_TRACE_MIN_BLOCKS
-#define SVDB_TRACE_MIN_BLOCKS 14 // <= 72 registers, 14.6 KB shared: 28 resident warps per SM
-#endif
-#ifndef SVDB_SCHED
-#define SVDB_SCHED 1 // 0: advance-to-point then gather; 1: per-iteration phase selection
-#endif
-#ifndef SVDB_W_SAMPLE_DEN
-#define SVDB_W_SAMPLE_DEN 1
-#endif
-#ifndef SVDB_W_SAMPLE
-#define SVDB_W_SAMPLE 1
-#endif
-#ifndef SVDB_CHUNK_MIN_SPP
-#define SVDB_CHUNK_MIN_SPP 16 // one GPU: whole-pixel items below this many samples per pixel
-#endif
-#ifndef SVDB_SPLIT_CHUNK
-#define SVDB_SPLIT_CHUNK 4 // max samples per work item when the frame is split over ranks
-#endif
-#ifndef SVDB_SAMPLE_CHUNK
-#define SVDB_SAMPLE_CHUNK 16 // max samples per work item (0: a lane owns a whole pixel)
-#endif
-#ifndef SVDB_SPEC_LOG
-#define SVDB_SPEC_LOG 1
-#endif
-#ifndef SVDB_FAST_EXIT
-#define SVDB_FAST_EXIT 0
-#endif
-#ifndef SVDB_ADV_ITERS
-#define SVDB_ADV_ITERS 3 // advance steps per advance-phase invocation
-#endif
-#ifndef SVDB_GATHER_ADV
-#define SVDB_GATHER_ADV 0
-#endif
-#ifndef SVDB_ADV_FRAC
-#define SVDB_ADV_FRAC 0 // > 0: stop early once fewer than nA / FRAC lanes still advance
-#endif
-#ifndef SVDB_W_START_NUM
-#define SVDB_W_START_NUM 1
-#define SVDB_W_START_DEN 1
-#endif
-#ifndef SVDB_COLD_SHARED
-#define SVDB_COLD_SHARED 1
-#endif
-#ifndef SVDB_SPEC_LOG_GATE
-#define SVDB_SPEC_LOG_GATE 0 // 1: skip the speculative log when the next cell is known empty (measured slower)
-#endif
-#ifndef SVDB_MAJ_AHEAD
-#define SVDB_MAJ_AHEAD 1
-#endif
-#ifndef SVDB_RAY_SHARED
-#define SVDB_RAY_SHARED 1
-#endif
-#ifndef SVDB_ACC_SHARED
-#define SVDB_ACC_SHARED 1
-#endif
-#ifndef SVDB_PERSIST_ACC_PT
-#define SVDB_PERSIST_ACC_PT 0 // 1: pathtrace keeps the accessor's caches between gathers
-#endif
-#ifndef SVDB_ACC_DIR_COLD
-#define SVDB_ACC_DIR_COLD 0
-#endif
 template <int CODEC, int MODE, bool CHUNK>
-__global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
+__global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
 {
-    extern __shared__ float4 s_ent[];
-    for (int i = threadIdx.x; i < A.tf.n; i += blockDim.x)
-        s_ent[i] = A.tf_ent[i];
-    __syncthreads();
+    extern __shared__ float4 s_tf[];
+    const float4* s_ent = stage_tf(A, s_tf);
     constexpr unsigned FULL = 0xffffffffu;
     constexpr bool RATIO = MODE == SVDBGPU_MODE_RATIO;
+    constexpr int T = kTraceThreads;
     const int lane = threadIdx.x & 31;
+    const int tid = threadIdx.x;
     unsigned long long* work = A.counters + 1;
 
     Tracer<CODEC> tr(A, s_ent);
     Rng rng{0};
-#if SVDB_RAY_SHARED
-    // the flight's ray is read only by the gather and written only at path start / scatter:
-    // kept in shared memory (SoA) so the advance loop does not hold its 12 registers
-    __shared__ double s_ray[6][SVDB_TRACE_THREADS];
+    // The flight's ray is read only by the gather and written only at path start / scatter: kept
+    // in shared memory (SoA) so the advance loop does not hold its 12 registers.
+    __shared__ double s_ray[6][T];
     auto ray_load = [&]() {
         Ray r;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            r.o[k] = reinterpret_cast<volatile double*>(s_ray[k])[threadIdx.x];
-            r.d[k] = reinterpret_cast<volatile double*>(s_ray[3 + k])[threadIdx.x];
+            r.o[k] = reinterpret_cast<volatile double*>(s_ray[k])[tid];
+            r.d[k] = reinterpret_cast<volatile double*>(s_ray[3 + k])[tid];
         }
         return r;
     };
     auto ray_store = [&](const Ray& r) {
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            reinterpret_cast<volatile double*>(s_ray[k])[threadIdx.x] = r.o[k];
-            reinterpret_cast<volatile double*>(s_ray[3 + k])[threadIdx.x] = r.d[k];
+            reinterpret_cast<volatile double*>(s_ray[k])[tid] = r.o[k];
+            reinterpret_cast<volatile double*>(s_ray[3 + k])[tid] = r.d[k];
         }
     };
-#else
-    Ray ray;
-    auto ray_load = [&]() { return ray; };
-    auto ray_store = [&](const Ray& r) { ray = r; };
-#endif
-#if SVDB_ACC_SHARED
-    // the accessor's node caches (frozen.hpp:228-277) are used only by the gather: shared memory
-    // between gathers, registers inside one
-    // No accessor state is kept between gathers: with the leaf directory a cold locate is one load
-    // (the leaf cache hit only ~5% of gathers), and dropping the 14 words per lane of shared memory
-    // and their registers lets 14 CTAs (28 warps) fit per SM instead of 12 (10 for ratio).
-    constexpr bool PERSIST_ACC = !RATIO && SVDB_PERSIST_ACC_PT;
-    __shared__ int s_acc[PERSIST_ACC ? 14 : 1][SVDB_TRACE_THREADS];
-    auto acc_io = [&](bool store) {
-        if constexpr (!PERSIST_ACC) {
-            if (!store)
-                tr.acc = Accessor<CODEC>(A.g);
-            return;
-        }
-        volatile int* p = &s_acc[0][threadIdx.x];
-        int* f[14] = {&tr.acc.lx, &tr.acc.ly, &tr.acc.lz, reinterpret_cast<int*>(&tr.acc.leaf),
-                      reinterpret_cast<int*>(&tr.acc.lo), reinterpret_cast<int*>(&tr.acc.sc),
-                      &tr.acc.wx, &tr.acc.wy, &tr.acc.wz, reinterpret_cast<int*>(&tr.acc.lower),
-                      &tr.acc.ux, &tr.acc.uy, &tr.acc.uz, &tr.acc.upper};
-#pragma unroll
-        for (int k = 0; k < 14; ++k) {
-            if (store)
-                p[k * SVDB_TRACE_THREADS] = *f[k];
-            else
-                *f[k] = p[k * SVDB_TRACE_THREADS];
-        }
-    };
-    acc_io(true);
-#endif
     // macrocell DDA state (23 words per lane) in shared memory, touched once per cell visit
-    __shared__ int s_dda_i[7][SVDB_TRACE_THREADS];
-    __shared__ double s_dda_d[8][SVDB_TRACE_THREADS];
-    SharedDda<SVDB_TRACE_THREADS> dda{&s_dda_i[0][0], &s_dda_d[0][0], int(threadIdx.x)};
-    auto dda_cur_index = [&]() { return dda.index(A.cells); };
-    double t = 0.0, tb = 0.0, inv = 0.0;
+    __shared__ int s_dda_i[7][T];
+    __shared__ double s_dda_d[8][T];
+    SharedDda<T> dda{&s_dda_i[0][0], &s_dda_d[0][0], tid};
+    // The step loop's live values stay in registers: t, the cell's far end tb, 1/majorant of this
+    // cell and of the next one (loaded one visit ahead), the RNG state.
+    double t = 0.0, tb = 0.0, inv = 0.0, inv_ahead = 0.0;
 #ifdef SVDB_PHASE_STATS
-    unsigned st_empty = 0, st_full = 0, st_leaf_hit = 0, st_lower_hit = 0;
+    unsigned st_empty = 0, st_full = 0;
 #endif
-#if SVDB_MAJ_AHEAD
-    double inv_ahead = 0.0;
-#endif
-#if SVDB_COLD_SHARED
     // Per-lane state touched only at sample start/end, scatter and pixel output lives in shared
-    // memory (SoA, conflict-free), keeping the step/gather loop's register footprint small.
-    // rows 0..6: acc0..2, tp0..2, t_ev; ratio tracking adds L0..2, Tr (pathtrace aliases those
-    // names to row 6, written only by the initialisation below, before t_ev)
-    __shared__ double s_cold_d[RATIO ? 11 : 7][SVDB_TRACE_THREADS];
-    __shared__ int s_cold_i[6 + (RATIO ? 1 : 0) + (CHUNK ? 1 : 0)][SVDB_TRACE_THREADS];
-    const int tid = threadIdx.x;
+    // memory (SoA, conflict-free). rows 0..6: acc0..2, tp0..2, t_ev; ratio tracking adds L0..2, Tr
+    // (pathtrace aliases those names to row 6, written only by the initialisation below, before t_ev)
+    __shared__ double s_cold_d[RATIO ? 11 : 7][T];
+    __shared__ int s_cold_i[6 + (RATIO ? 1 : 0) + (CHUNK ? 1 : 0)][T];
     volatile double &acc0 = s_cold_d[0][tid], &acc1 = s_cold_d[1][tid], &acc2 = s_cold_d[2][tid];
     volatile double &tp0 = s_cold_d[3][tid], &tp1 = s_cold_d[4][tid], &tp2 = s_cold_d[5][tid];
     volatile double& t_ev = s_cold_d[6][tid];
     constexpr int kR0 = RATIO ? 7 : 6, kR = RATIO ? 1 : 0;
     volatile double &L0 = s_cold_d[kR0][tid], &L1 = s_cold_d[kR0 + kR][tid], &L2 = s_cold_d[kR0 + 2 * kR][tid];
-    volatile double &Tr = s_cold_d[kR0 + 3 * kR][tid];
+    volatile double& Tr = s_cold_d[kR0 + 3 * kR][tid];
     volatile int& have_d = s_cold_i[RATIO ? 6 : 0][tid];              // ratio: event pending (0/1)
     volatile int& s_end = s_cold_i[CHUNK ? (RATIO ? 7 : 6) : 0][tid]; // chunked: end of the lane's samples
     volatile int &px = s_cold_i[0][tid], &py = s_cold_i[1][tid], &s = s_cold_i[2][tid];
@@ -820,16 +652,6 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
     if constexpr (CHUNK)
         s_end = 0;
     v_ev = 0.0f;
-#else
-    int px = 0, py = 0, s = 0;
-    long long out_off = 0;
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-    double tp0 = 1.0, tp1 = 1.0, tp2 = 1.0;
-    int bounces = 0;
-    double L0 = 0.0, L1 = 0.0, L2 = 0.0, Tr = 1.0, t_ev = 0.0; // ratio tracking
-    float v_ev = 0.0f;
-    bool have = false;
-#endif
     int state = kNeedPixel;
     bool done = false;
     long long unit = 0;
@@ -882,15 +704,9 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
                     finish_path(0.0f, 0.0f, 0.0f);
                 return;
             }
-#if SVDB_COLD_SHARED
 #pragma unroll 1
             for (int k = 0; k < 3; ++k) // one division site (render.hpp:184)
                 s_cold_d[3 + k][tid] /= survive;
-#else
-            tp0 /= survive;
-            tp1 /= survive;
-            tp2 /= survive;
-#endif
         }
         state = kNeedSegment;
     };
@@ -909,8 +725,8 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
                         float(tp2 * double(A.ambient[2])));
         }
     };
-    // kNeedPath / kNeedSegment: write a finished pixel, start the next sample (render.hpp:298-302),
-    // or enter the macrocell DDA with a new flight (render.hpp:142)
+    // kScatter / kNeedPath / kNeedSegment: scatter, write a finished pixel, start the next sample
+    // (render.hpp:298-302), or enter the macrocell DDA with a new flight (render.hpp:142)
     auto do_start = [&]() {
         if (state == kScatter) { // the only copy of the scattering code in the loop
             bounce(t_ev, v_ev);
@@ -925,15 +741,9 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
                 }
             }
             if (s == A.spp) {
-#if SVDB_COLD_SHARED
 #pragma unroll 1
                 for (int k = 0; k < 3; ++k) // render.hpp:308-310, one division site
                     A.out[out_off + k] = float(s_cold_d[k][tid] / double(A.spp));
-#else
-                A.out[out_off] = float(acc0 / double(A.spp));
-                A.out[out_off + 1] = float(acc1 / double(A.spp));
-                A.out[out_off + 2] = float(acc2 / double(A.spp));
-#endif
                 state = kNeedPixel;
                 return;
             }
@@ -963,46 +773,29 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             end_segment();
             return;
         }
-#if SVDB_MAJ_AHEAD
-        inv_ahead = __ldg(A.inv_maj + dda_cur_index());
-#endif
+        inv_ahead = __ldg(A.inv_maj + dda.index(A.cells));
         state = kNeedCell;
     };
     // kNeedCell -> next macrocell (empty cells draw nothing, render.hpp:145-146);
     // kInCell -> one tentative step t -= ln(1-u)/sigma_maj (render.hpp:116-118)
-    auto do_advance = [&](auto& D) {
-#if SVDB_SPEC_LOG
+    auto do_advance = [&]() {
         // the step draw's log does not depend on the DDA: compute it from the next uniform before
         // the cell lookup (independent FP64 chains interleave); the draw is consumed only if the
         // cell has draws, so the stream is unchanged
-#if SVDB_SPEC_LOG_GATE && SVDB_MAJ_AHEAD
-        // a lane about to enter a cell whose majorant (loaded one visit ahead) is 0 draws nothing
-        // there: skip its log, so warps whose advancing lanes all cross empty cells skip it
-        const double lg = (state == kInCell || inv_ahead > 0.0) ? step_log(1.0 - rng.peek()) : 0.0;
-#else
         const double lg = step_log(1.0 - rng.peek());
-#endif
-#endif
         if (state == kNeedCell) {
             int c[3];
             double ta, tbb;
-            if ((RATIO && !(Tr > 0.0)) || !D.next(A.cells, c, ta, tbb)) {
+            if ((RATIO && !(Tr > 0.0)) || !dda.next(A.cells, c, ta, tbb)) {
                 end_segment();
                 return;
             }
             // 1.0 / double(majorant) precomputed per cell with the same IEEE division
-            // (render.hpp:113); 0 marks an empty cell
-#ifdef SVDB_SOL_NO_MAJ_LOAD // speed-of-light experiment only (wrong images): no majorant load
-            inv = 1.0 / 0.02;
-#elif SVDB_MAJ_AHEAD
-            // the majorant of this cell was loaded one visit ahead; issue the next cell's now
-            // (dda.c already holds the following cell) so the load overlaps a whole iteration
+            // (render.hpp:113), 0 marks an empty cell. This cell's was loaded one visit ahead;
+            // issue the next cell's now so the load overlaps a whole iteration.
             inv = inv_ahead;
-            if (!D.done())
-                inv_ahead = __ldg(A.inv_maj + D.index(A.cells));
-#else
-            inv = __ldg(A.inv_maj + tr.cell_index(c));
-#endif
+            if (!dda.done())
+                inv_ahead = __ldg(A.inv_maj + dda.index(A.cells));
 #ifdef SVDB_PHASE_STATS
             ++(inv > 0.0 ? st_full : st_empty);
 #endif
@@ -1011,27 +804,8 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             t = ta;
             tb = tbb;
         }
-#if SVDB_FAST_EXIT
-        // Most draws leave the cell, and then only the decision t_new >= tb is used, never t_new.
-        // Decide it from a float lower bound of -ln(w) (MUFU lg2: |error| <= 4e-7 (1 + y), bound
-        // taken 10x wider) when the bound already clears the gap; the FP64 log runs only for
-        // collisions and near-ties, so every decision and collision point equals the exact path's.
-        const double w = 1.0 - rng.uniform(); // exact: u is a multiple of 2^-53
-        {
-            const float y = -__log2f(float(w)) * 0.693147182f;
-            const float y_lb = y - (4e-6f + 4e-6f * y);
-            if (y_lb * float(inv) * 0.999999f > float(tb - t) * 1.000001f) {
-                state = kNeedCell;
-                return;
-            }
-        }
-        t -= log(w) * inv;
-#elif SVDB_SPEC_LOG
         rng.skip();
         t -= lg * inv;
-#else
-        t -= step_log(1.0 - rng.uniform()) * inv;
-#endif
         state = t >= tb ? kNeedCell : kPoint;
     };
     // accept test on the gathered value (render.hpp:119-122) / ratio update
@@ -1059,46 +833,15 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             }
         }
     };
-    // kPoint: trilinear gather at the tentative collision + accept test (render.hpp:119-122)
+    // kPoint: trilinear gather at the tentative collision + accept test (render.hpp:119-122). No
+    // accessor state is kept between gathers: with the leaf directory a cold locate is one load.
     auto do_sample = [&]() {
-#ifdef SVDB_SOL_NO_GATHER // speed-of-light experiment only (wrong images): no voxel memory
-        float v = float(t * 1e-3 - floor(t * 1e-3));
-        ++tr.samples;
-#else
-#if SVDB_ACC_SHARED
-#if SVDB_ACC_DIR_COLD
-        // with a leaf directory every leaf-cache miss is one load: start each gather from a cold
-        // accessor instead of saving / restoring its 14 words (the leaf cache hits ~5% in C3)
-        if (A.g.dir)
-            tr.acc = Accessor<CODEC>(A.g);
-        else
-#endif
-            acc_io(false);
-#endif
-#ifdef SVDB_PHASE_STATS
-        {
-            const Ray rr = ray_load();
-            const int qx = lattice_coord(rr.o[0] + rr.d[0] * t), qy = lattice_coord(rr.o[1] + rr.d[1] * t),
-                      qz = lattice_coord(rr.o[2] + rr.d[2] * t);
-            if (tr.acc.in_leaf(qx, qy, qz))
-                ++st_leaf_hit;
-            else if (tr.acc.in_lower(qx, qy, qz))
-                ++st_lower_hit;
-        }
-#endif
-        float v = tr.sample_at(ray_load(), t);
-#if SVDB_ACC_SHARED
-#if SVDB_ACC_DIR_COLD
-        if (!A.g.dir)
-#endif
-            acc_io(true);
-#endif
-#endif
-        accept(v);
+        tr.acc = Accessor<CODEC>(A.g);
+        accept(tr.sample_at(ray_load(), t));
     };
 
     for (;;) {
-        // ---- hand out pixels (warp-uniform point) ----
+        // ---- hand out work items (warp-uniform point) ----
         unsigned need = __ballot_sync(FULL, state == kNeedPixel && !done);
         while (need) {
             if (fill >= 32) {
@@ -1151,83 +894,29 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
             break;
         if (done)
             continue; // finished lanes idle until the whole warp is done
-#if SVDB_SCHED == 1
-        // ---- phase selection: run the one phase most lanes are waiting in (weights favour
-        // the gather so its memory latency is paid by as many lanes as possible at once) ----
-        {
-            const int nS = __popc(__ballot_sync(live, state == kPoint));
-            const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell));
-            const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter));
-            // start lanes may wait to batch up, but a non-empty phase is always chosen
-            const int nTw = nT > 0 ? max(1, nT * SVDB_W_START_NUM / SVDB_W_START_DEN) : 0;
-            const int nSw = nS * SVDB_W_SAMPLE / SVDB_W_SAMPLE_DEN;
-            const int phase = (nS > 0 && nSw >= nA && nSw >= nTw) || (nA == 0 && nTw == 0) ? 2 : (nA >= nTw ? 1 : 0);
+        // ---- phase selection: run the one phase most lanes are waiting in; ties go to the
+        // gather so its memory latency is paid by as many lanes as possible at once ----
+        const int nS = __popc(__ballot_sync(live, state == kPoint));
+        const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell));
+        const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter));
+        const int phase = (nS > 0 && nS >= nA && nS >= nT) || (nA == 0 && nT == 0) ? 2 : (nA >= nT ? 1 : 0);
 #ifdef SVDB_PHASE_STATS
-            if (lane == __ffs(live) - 1) { // per phase: invocations and participating lanes
-                const int n = phase == 0 ? nT : (phase == 1 ? nA : nS);
-                atomicAdd(A.counters + 2 + 2 * phase, 1ull);
-                atomicAdd(A.counters + 3 + 2 * phase, (unsigned long long)n);
-            }
-#endif
-#ifdef SVDB_PHASE_STATS
-            __syncwarp(live);
-            const long long c0 = clock64();
-#endif
-            if (phase == 0) {
-                if (state == kNeedPath || state == kNeedSegment || state == kScatter)
-                    do_start();
-            } else if (phase == 1) {
-#if SVDB_ADV_FRAC
-                // keep advancing while enough of the phase's lanes are still advancing
-                for (int k = 0;; ++k) {
-                    const bool adv = state == kNeedCell || state == kInCell;
-                    const int n = __popc(__ballot_sync(live, adv));
-                    if (n == 0 || k >= SVDB_ADV_ITERS || n * SVDB_ADV_FRAC < nA)
-                        break;
-                    if (adv)
-                        do_advance(dda);
-                }
-#else
-#if SVDB_DDA_REGS
-                if (state == kNeedCell || state == kInCell) {
-                    // the DDA's moving state lives in registers for the whole advance phase
-                    DdaRegs<SVDB_TRACE_THREADS> R;
-                    R.load(dda);
-#pragma unroll 1
-                    for (int k = 0; k < SVDB_ADV_ITERS && (state == kNeedCell || state == kInCell); ++k)
-                        do_advance(R);
-                    R.store();
-                }
-#else
-#pragma unroll 1
-                for (int k = 0; k < SVDB_ADV_ITERS && (state == kNeedCell || state == kInCell); ++k)
-                    do_advance(dda);
-#endif
-#endif
-            } else if (state == kPoint) {
-                do_sample();
-#pragma unroll 1
-                for (int k = 0; k < SVDB_GATHER_ADV && (state == kNeedCell || state == kInCell); ++k)
-                    do_advance(dda); // rejected collisions draw their next step at once
-            }
-#ifdef SVDB_PHASE_STATS
-            __syncwarp(live);
-            if (lane == __ffs(live) - 1)
-                atomicAdd(A.counters + 8 + phase, (unsigned long long)(clock64() - c0));
-#endif
+        if (lane == __ffs(live) - 1) { // per phase: invocations and participating lanes
+            const int n = phase == 0 ? nT : (phase == 1 ? nA : nS);
+            atomicAdd(A.counters + 2 + 2 * phase, 1ull);
+            atomicAdd(A.counters + 3 + 2 * phase, (unsigned long long)n);
         }
-#else
-        // ---- divergent advance (ALU only) to the next tentative collision, then one
-        // re-converged gather + accept for every lane that has a point ----
-        while (state != kNeedPixel && state != kPoint) {
+#endif
+        if (phase == 0) {
             if (state == kNeedPath || state == kNeedSegment || state == kScatter)
                 do_start();
-            else
-                do_advance(dda);
-        }
-        if (state == kPoint)
+        } else if (phase == 1) {
+#pragma unroll 1
+            for (int k = 0; k < kAdvIters && (state == kNeedCell || state == kInCell); ++k)
+                do_advance();
+        } else if (state == kPoint) {
             do_sample();
-#endif
+        }
     }
     unsigned long long s64 = tr.samples;
 #pragma unroll
@@ -1238,8 +927,6 @@ __global__ void __launch_bounds__(SVDB_TRACE_THREADS, SVDB_TRACE_MIN_BLOCKS) k_t
 #ifdef SVDB_PHASE_STATS
     atomicAdd(A.counters + 12, (unsigned long long)st_empty); // macrocell visits: empty / non-empty
     atomicAdd(A.counters + 13, (unsigned long long)st_full);
-    atomicAdd(A.counters + 14, (unsigned long long)st_leaf_hit); // gathers: leaf-cache hits
-    atomicAdd(A.counters + 15, (unsigned long long)st_lower_hit); // leaf miss, lower-cache hit
 #endif
 }
 
@@ -1417,7 +1104,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     A.packed = packed;
     A.counters = g->d_counters;
     const int64_t ntiles = tiles_for_rank(cam->width, cam->height, rank, nranks);
-    const size_t smem = sizeof(float4) * size_t(tf->n_entries);
+    const size_t smem = tf_smem_bytes(tf->n_entries);
     cudaEvent_t e2 = nullptr, e3 = nullptr;
     SVDB_CUDA(cudaEventCreate(&e2));
     SVDB_CUDA(cudaEventCreate(&e3));
@@ -1434,8 +1121,8 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         // one GPU: items of up to 16 samples, at least 2 per pixel, from 16 spp up (C3: 4 per pixel,
         // C2 / C4: 2); fewer spp keep whole pixels, whose tail is already short. Split frames
         // (N ranks, 1/N of the work each) use 4 so the tail stays small against the shorter frame
-        const int chunk = nranks > 1 ? std::min(SVDB_SPLIT_CHUNK, std::max(1, st->spp / 2))
-                                     : (st->spp >= SVDB_CHUNK_MIN_SPP ? std::min(SVDB_SAMPLE_CHUNK, st->spp / 2) : 0);
+        const int chunk = nranks > 1 ? std::min(kSplitChunk, std::max(1, st->spp / 2))
+                                     : (st->spp >= kChunkMinSpp ? std::min(kSampleChunk, st->spp / 2) : 0);
         const size_t npix = packed ? size_t(ntiles) * 256 : size_t(cam->width) * size_t(cam->height);
         const size_t bytes = npix * size_t(st->spp) * 3 * sizeof(float);
         if (chunk > 0 && chunk < st->spp && bytes <= (size_t(8) << 30)) {
@@ -1460,9 +1147,9 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     {                                                                                          \
         int per_sm = 1;                                                                        \
         auto kern = A.chunk ? k_trace<C, M, true> : k_trace<C, M, false>;                         \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SVDB_TRACE_THREADS, smem);       \
-        long long blocks = std::min<long long>((long long)std::max(per_sm, 1) * sms, (n_units * 32 + SVDB_TRACE_THREADS - 1) / SVDB_TRACE_THREADS); \
-        kern<<<unsigned(blocks), SVDB_TRACE_THREADS, smem, s>>>(A, n_units);                          \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTraceThreads, smem);       \
+        long long blocks = std::min<long long>((long long)std::max(per_sm, 1) * sms, (n_units * 32 + kTraceThreads - 1) / kTraceThreads); \
+        kern<<<unsigned(blocks), kTraceThreads, smem, s>>>(A, n_units);                          \
     }
 #define LAUNCH_R(C, M) k_render<C, M><<<unsigned(ntiles), 256, smem, s>>>(A)
 #define BY_MODE(C)                                                                             \
@@ -1508,12 +1195,10 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         cudaMemcpy(c, g->d_counters, 128, cudaMemcpyDeviceToHost);
         const char* names[3] = {"start", "advance", "gather"};
         fprintf(stderr, "[phase-stats] macrocell visits: empty %llu non-empty %llu\n", c[12], c[13]);
-        fprintf(stderr, "[phase-stats] gathers %llu: leaf-cache hits %llu, lower-cache hits %llu\n", samples, c[14],
-                c[15]);
+        fprintf(stderr, "[phase-stats] gathers %llu\n", samples);
         for (int p = 0; p < 3; ++p)
-            fprintf(stderr, "[phase-stats] %-8s invocations %llu lanes/invocation %.2f cycles/invocation %.1f\n",
-                    names[p], c[2 + 2 * p], c[2 + 2 * p] ? double(c[3 + 2 * p]) / double(c[2 + 2 * p]) : 0.0,
-                    c[2 + 2 * p] ? double(c[8 + p]) / double(c[2 + 2 * p]) : 0.0);
+            fprintf(stderr, "[phase-stats] %-8s invocations %llu lanes/invocation %.2f\n", names[p], c[2 + 2 * p],
+                    c[2 + 2 * p] ? double(c[3 + 2 * p]) / double(c[2 + 2 * p]) : 0.0);
     }
 #endif
     float rms = 0.0f, mms = 0.0f;

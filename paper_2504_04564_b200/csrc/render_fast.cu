@@ -23,33 +23,15 @@
 #include <algorithm>
 #include <type_traits>
 
-#ifndef SVDB_MIX_ACCEPT64
-#define SVDB_MIX_ACCEPT64 0
-#endif
-#ifndef SVDB_MIX_SAMPLE64
-#define SVDB_MIX_SAMPLE64 0
-#endif
 
 namespace svdbgpu {
 
 namespace {
 
 constexpr int kT = 64;          // threads per CTA
-#ifndef SVDB_F_MIN_BLOCKS_MIXED
-#define SVDB_F_MIN_BLOCKS_MIXED 14
-#endif
-#ifndef SVDB_F_PERSIST_ACC
-#define SVDB_F_PERSIST_ACC 0 // accessor caches kept between gathers (off: cold locate = one directory load)
-#endif
-#ifndef SVDB_F_REBASE
-#define SVDB_F_REBASE 0 // FP32: camera ray built and clipped in FP64, origin moved to the volume entry (measured: DESIGN.md §3.4)
-#endif
-#ifndef SVDB_F_ADV_ITERS
-#define SVDB_F_ADV_ITERS 3
-#endif
 constexpr int kMinBlocks = 16;                           // 32 warps per SM (pure FP32)
-constexpr int kMinBlocksMixed = SVDB_F_MIN_BLOCKS_MIXED; // FP64 geometry: 212 B of shared state per lane
-constexpr int kAdvIters = SVDB_F_ADV_ITERS;              // advance steps per advance-phase invocation
+constexpr int kMinBlocksMixed = 14; // FP64 geometry: 212 B of shared state per lane
+constexpr int kAdvIters = 3;       // advance steps per advance-phase invocation
 constexpr unsigned kFull = 0xffffffffu;
 
 enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4, kPoint = 5, kScatter = 6 };
@@ -177,41 +159,6 @@ __device__ __forceinline__ RayG<G> camera_ray_g(const CamArgs& c, G px, G py)
     return r;
 }
 
-// FP32 geometry: the camera ray in FP64 (53-bit jitter), clipped to [0, hi] (dda.hpp:25-46) and
-// restarted at the entry point, so the float distances t along the first segment start near 0
-// instead of at the camera distance (C4: ~2,000-4,000 voxels, where a float t is off by ~2e-4)
-__device__ __forceinline__ RayG<float> camera_ray_entry(const CamArgs& c, double px, double py, const double hi[3])
-{
-    const RayG<double> r = camera_ray_g<double>(c, px, py);
-    double t0 = 0.0, t1 = __longlong_as_double(0x7ff0000000000000ll);
-    bool hit = true;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        if (r.d[a] == 0.0) {
-            hit = hit && !(r.o[a] < 0.0 || r.o[a] > hi[a]);
-            continue;
-        }
-        const double inv = 1.0 / r.d[a];
-        double ta = (0.0 - r.o[a]) * inv, tb = (hi[a] - r.o[a]) * inv;
-        if (ta > tb) {
-            const double tt = ta;
-            ta = tb;
-            tb = tt;
-        }
-        t0 = fmax(t0, ta);
-        t1 = fmin(t1, tb);
-    }
-    if (!(hit && t0 <= t1))
-        t0 = 0.0; // a miss stays a miss from the camera
-    RayG<float> f;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        f.o[a] = float(r.o[a] + r.d[a] * t0);
-        f.d[a] = float(r.d[a]);
-    }
-    return f;
-}
-
 // Macrocell DDA (dda.hpp:25-109) in float, per-lane state in shared memory (SoA)
 template <typename G>
 struct SharedDdaG {
@@ -301,10 +248,15 @@ template <int CODEC, int MODE, typename G, bool CHUNK>
 __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMixed)
     k_trace_f(const __grid_constant__ RenderArgs A, long long n_units)
 {
-    extern __shared__ float4 s_ent[];
-    for (int i = threadIdx.x; i < A.tf.n; i += blockDim.x)
-        s_ent[i] = A.tf_ent[i];
-    __syncthreads();
+    extern __shared__ float4 s_tf[];
+    const float4* s_ent = s_tf;
+    if (A.tf.n > kTfSmemMax) { // large tables are read in place (L1-cached)
+        s_ent = A.tf_ent;
+    } else {
+        for (int i = threadIdx.x; i < A.tf.n; i += blockDim.x)
+            s_tf[i] = A.tf_ent[i];
+        __syncthreads();
+    }
     constexpr bool RATIO = MODE == SVDBGPU_MODE_RATIO;
     const int lane = threadIdx.x & 31;
     const int tid = threadIdx.x;
@@ -322,8 +274,6 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
     __shared__ G s_tev[kT];
     // no accessor state between gathers (cold locate = one directory load): its per-lane state
     // would otherwise cost CTAs per SM
-    constexpr bool PERSIST_ACC = SVDB_F_PERSIST_ACC != 0;
-    __shared__ int s_acc[PERSIST_ACC ? 14 : 1][kT];
     __shared__ double s_sum[3][kT];                    // per-pixel FP64 accumulation
     __shared__ float s_cold[RATIO ? 8 : 5][kT];        // tp0..2, (unused), v_ev (+ L0..2)
     // ratio transmittance stays FP64: a float product underflows to 0 (ending the flight) long
@@ -343,25 +293,6 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
     volatile int& s_end = ci[(CHUNK ? (RATIO ? 6 : 5) : 0) * kT]; // chunked: end of the lane's samples
 
     Accessor<CODEC> acc(A.g);
-    auto acc_io = [&](bool store) {
-        if constexpr (!PERSIST_ACC) {
-            if (!store)
-                acc = Accessor<CODEC>(A.g);
-            return;
-        }
-        volatile int* p = &s_acc[0][tid];
-        int* f[14] = {&acc.lx, &acc.ly, &acc.lz, reinterpret_cast<int*>(&acc.leaf), reinterpret_cast<int*>(&acc.lo),
-                      reinterpret_cast<int*>(&acc.sc), &acc.wx, &acc.wy, &acc.wz, reinterpret_cast<int*>(&acc.lower),
-                      &acc.ux, &acc.uy, &acc.uz, &acc.upper};
-#pragma unroll
-        for (int k = 0; k < 14; ++k) {
-            if (store)
-                p[k * kT] = *f[k];
-            else
-                *f[k] = p[k * kT];
-        }
-    };
-    acc_io(true);
     auto ray_load = [&]() {
         Ray r;
 #pragma unroll
@@ -381,9 +312,8 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
 
     RngF rng{0};
     constexpr bool MIXED = sizeof(G) == 8;
-    constexpr bool ACC64 = MIXED && SVDB_MIX_ACCEPT64; // accept test in FP64 as the reference
-    using I = typename std::conditional<ACC64, double, float>::type;
-    const I* inv_tab = reinterpret_cast<const I*>(ACC64 ? (const void*)A.inv_maj : (const void*)A.inv_maj_f);
+    using I = float;
+    const I* inv_tab = A.inv_maj_f;
     G t = G(0), tb = G(0);
     I inv = I(0), inv_ahead = I(0);
     uint32_t samples = 0;
@@ -506,20 +436,14 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
                 rng.state = r0.state;
             }
             G jx, jy;
-            if constexpr (!MIXED && SVDB_F_REBASE) {
-                const double djx = rng.uniform53(), djy = rng.uniform53();
-                const double dhi[3] = {A.hi[0], A.hi[1], A.hi[2]};
-                ray_store(camera_ray_entry(A.cam, double(px) + djx, double(py) + djy, dhi));
-                jx = jy = G(0);
-            } else if constexpr (MIXED) {
+            if constexpr (MIXED) {
                 jx = rng.uniform53();
                 jy = rng.uniform53();
             } else {
                 jx = rng.uniform();
                 jy = rng.uniform();
             }
-            if constexpr (MIXED || !SVDB_F_REBASE)
-                ray_store(camera_ray_g<G>(A.cam, G(px) + jx, G(py) + jy));
+            ray_store(camera_ray_g<G>(A.cam, G(px) + jx, G(py) + jy));
             tp(0) = tp(1) = tp(2) = 1.0f;
             bounces = 0;
             if constexpr (RATIO)
@@ -560,16 +484,6 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
         state = t >= tb ? kNeedCell : kPoint;
     };
     auto accept = [&](float v) {
-        if constexpr (ACC64 && !RATIO) { // render.hpp:119-122 in FP64 with the 53-bit draw
-            if (rng.uniform53() < tf_extinction(A.tf, s_ent, double(v)) * inv) {
-                t_ev = t;
-                v_ev = v;
-                state = kScatter;
-            } else {
-                state = kInCell;
-            }
-            return;
-        }
         const float st = tf.extinction(v);
         if constexpr (RATIO) {
             const float r = float(st * inv);
@@ -595,17 +509,10 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
         }
     };
     auto do_sample = [&]() {
-        acc_io(false);
+        acc = Accessor<CODEC>(A.g); // no accessor state between gathers (cold locate = one directory load)
         const Ray r = ray_load();
         ++samples;
-        float v;
-        if constexpr (MIXED && SVDB_MIX_SAMPLE64) // the reference's FP64 trilinear (sample.hpp:46-72)
-            v = sample_trilinear<CODEC>(acc, double(r.o[0] + r.d[0] * t), double(r.o[1] + r.d[1] * t),
-                                        double(r.o[2] + r.d[2] * t));
-        else
-            v = sample_f<CODEC, G>(acc, r.o[0] + r.d[0] * t, r.o[1] + r.d[1] * t, r.o[2] + r.d[2] * t);
-        acc_io(true);
-        accept(v);
+        accept(sample_f<CODEC, G>(acc, r.o[0] + r.d[0] * t, r.o[1] + r.d[1] * t, r.o[2] + r.d[2] * t));
     };
 
     for (;;) {

@@ -168,7 +168,29 @@ int main()
         float b = gpu::sample(*slot, Vec3d{16.25, 16.5, 16.75}, SampleMode::trilinear);
         Accessor acc(*slot);
         report("grid_cache_revalidates", b == sample(acc, Vec3d{16.25, 16.5, 16.75}, SampleMode::trilinear) && a != b);
+        gpu::GridCache::evict(*slot);
         delete slot;
+    }
+
+    // 7b. GridCache is bounded (LRU by device bytes) and evictable; a held grid outlives eviction
+    {
+        gpu::GridCache::clear();
+        FrozenGrid g1 = compress(synth_blobs({32, 32, 32}, 5, 3), CompressionParams{}).first;
+        FrozenGrid g2 = compress(synth_blobs({40, 40, 40}, 6, 4), CompressionParams{}).first;
+        std::shared_ptr<gpu::Grid> h1 = gpu::GridCache::get(g1, gpu::Codec::f32);
+        const uint64_t one = gpu::GridCache::resident_bytes();
+        const uint64_t old_budget = gpu::GridCache::budget();
+        gpu::GridCache::set_budget(one); // room for one grid only
+        std::shared_ptr<gpu::Grid> h2 = gpu::GridCache::get(g2, gpu::Codec::f32);
+        const bool lru = gpu::GridCache::size() == 1;
+        // h1 was evicted from the cache but is still usable through the shared handle
+        float v = gpu::sample(*h1, gpu::Vec3d{16.25, 16.5, 16.75}, gpu::SampleMode::trilinear);
+        Accessor acc1(g1);
+        const bool alive = v == sample(acc1, Vec3d{16.25, 16.5, 16.75}, SampleMode::trilinear);
+        gpu::GridCache::evict(g2);
+        const bool evicted = gpu::GridCache::size() == 0 && gpu::GridCache::resident_bytes() == 0;
+        gpu::GridCache::set_budget(old_budget);
+        report("grid_cache_bounded_lru_evict", lru && alive && evicted);
     }
 
     // 4. error mapping: corrupt containers raise the reference's Errc

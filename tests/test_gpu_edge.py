@@ -171,3 +171,37 @@ def test_packed_device_split_and_unpack_match_reference(gpu, ref, spp):
     torch.cuda.synchronize()
     got = frame.cpu().numpy().reshape(cam.height, cam.width, 3)
     _check(got, want, min_same=0.98)
+
+
+@pytest.mark.parametrize("n_entries", [1025, 4096])
+@pytest.mark.parametrize("mode", [P.RenderMode.pathtrace, P.RenderMode.ratio])
+def test_large_transfer_function_reads_global(gpu, ref, orc, n_entries, mode):
+    # TFs above kTfSmemMax (1024) entries are read from global memory instead of shared memory; any
+    # entry count the reference accepts renders (a 4096-entry LUT used to fail to launch)
+    svdb = _tile_grid(ref, dims=(40, 36, 33), background=0.1, seed=31)
+    r = SplitMix(n_entries)
+    ent = [[r.uniform(), r.uniform(), r.uniform(), r.uniform()] for _ in range(n_entries)]
+    tf = P.TransferFunction(0.0, 1.0, ent, 0.05)
+    g = P.DeviceGrid(svdb, P.Codec.f32)
+    maj = g.macrocells(tf)[3]
+    want_maj = ref.open(svdb).macrocells(tf)[3]
+    assert np.array_equal(maj.view(np.uint32), want_maj.view(np.uint32))
+    cam = P.Camera(position=(19.5, 60.0, -50.0), look_at=(19.5, 17.5, 16.0), width=24, height=20)
+    st = P.RenderSettings(spp=2, seed=9, mode=mode)
+    img = P.render(g, tf, cam, st).pixels
+    want = (ref.open(svdb).render(tf, cam, st) if mode == P.RenderMode.pathtrace
+            else orc.open(svdb).render(tf, cam, st)[0])
+    _check(img, want)
+
+
+def test_rank_with_no_tiles_succeeds(gpu, ref):
+    # a 16x16 frame has one tile: ranks 1..3 of 4 own nothing and must render nothing, successfully
+    svdb = _tile_grid(ref, dims=(24, 24, 24), background=0.0, seed=3)
+    g = P.DeviceGrid(svdb, P.Codec.f32)
+    cam = P.Camera(position=(11.5, 40.0, -30.0), look_at=(11.5, 11.5, 11.5), width=16, height=16)
+    st = P.RenderSettings(spp=2, seed=1)
+    for r in range(1, 4):
+        img = P.render(g, TF, cam, st, tile_rank=r, tile_nranks=4)
+        assert img.stats["paths"] == 0
+    with pytest.raises(P.Error):
+        P.render(g, TF, cam, st, tile_rank=4, tile_nranks=4)
