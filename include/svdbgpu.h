@@ -101,7 +101,9 @@ typedef struct {
                                 (bit-parity mode); 128 = lower-node, 8 = leaf-node majorants
                                 (node-majorant tracking; statistically equal, different streams) */
     int32_t precision;       /* SVDBGPU_PRECISION_*: tracking arithmetic (pathtrace / ratio) */
-    int32_t reserved[1];
+    int32_t hdda;            /* 1: hierarchical DDA — empty 128^3 lower-node regions are skipped in one
+                                coarse step, the majorant grid is walked inside non-empty ones
+                                (pathtrace / ratio, FP64; statistically equal, different streams) */
 } svdbgpu_settings;
 
 typedef struct {

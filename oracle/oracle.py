@@ -116,9 +116,28 @@ class Oracle:
         L.so_mix64.restype = C.c_uint64
         L.so_rng_uniforms.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_size_t, C.c_void_p]
         L.so_free.argtypes = [C.c_void_p]
+        L.so_synth.argtypes = [C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p]
+        L.so_sparse_threshold.argtypes = [C.c_int]
+        L.so_sparse_threshold.restype = C.c_double
 
     def open(self, svdb: bytes) -> "OracleGrid":
         return OracleGrid(self, svdb)
+
+    SYNTH_KINDS = {"marschner_lobb": 0, "fbm_smoke": 1, "turbulence": 2, "sparse": 3}
+
+    def synth(self, kind, dims, seed: int = 0, threads: int = 0) -> np.ndarray:
+        """Restated synthetic volume [z, y, x] float32 (synth_oracle.c), bit-identical to the
+        product's svdbgpu_synth, so baselines can build inputs without the product library."""
+        k = self.SYNTH_KINDS[kind] if isinstance(kind, str) else int(kind)
+        dx, dy, dz = (int(d) for d in dims)
+        out = np.empty((dz, dy, dx), dtype=np.float32)
+        rc = self.lib.so_synth(k, (C.c_int32 * 3)(dx, dy, dz), seed, threads, out.ctypes.data)
+        if rc:
+            raise OracleError(rc, "synth")
+        return out
+
+    def sparse_threshold(self, dim_max: int) -> float:
+        return self.lib.so_sparse_threshold(dim_max)
 
     def quantize(self, svdb: bytes, codec: int):
         """-> (dequantised svdb bytes, codes[n_leaf,512] u8, params[n_leaf,2] f32)."""
@@ -244,7 +263,7 @@ class Reference:
                                        C.c_double, C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_int,
                                        C.c_int, C.c_int, C.c_uint64, C.c_void_p, C.c_int, C.c_int,
                                        C.c_int, C.c_void_p, C.POINTER(C.c_uint64),
-                                       C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+                                       C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.c_int]
         L.ref_woodcock.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_void_p, C.c_int,
                                    C.c_double, C.c_double, C.c_void_p, C.c_double, C.c_double,
                                    C.c_uint64, C.c_size_t, C.c_void_p, C.POINTER(C.c_uint64)]
@@ -372,9 +391,11 @@ class RefGrid:
             threads, rgb.ctypes.data), "render")
         return rgb
 
-    def render_tiles(self, tf, cam, settings, tile_stride=1, tile_phase=0, threads=0, rgb=None):
+    def render_tiles(self, tf, cam, settings, tile_stride=1, tile_phase=0, threads=0, rgb=None,
+                     count=True):
         """Reference per-pixel body over a tile subset (needs macrocells(tf) first).
-        -> (rgb, lookups, paths, seconds)."""
+        -> (rgb, lookups, paths, seconds). count=False traces through the stock GridField (no
+        per-lookup counter in the timed loop) and returns lookups = 0."""
         ent = tf_entries(tf)
         if rgb is None:
             rgb = np.zeros((cam.height, cam.width, 3), dtype=np.float32)
@@ -384,7 +405,7 @@ class RefGrid:
             _cam9(cam), cam.fov_y_deg, cam.width, cam.height, settings.spp, settings.max_bounces,
             settings.rr_start_bounce, settings.seed, (C.c_float * 3)(*settings.ambient_radiance),
             threads, tile_stride, tile_phase, rgb.ctypes.data, C.byref(lk), C.byref(pa),
-            C.byref(sec)), "render_tiles")
+            C.byref(sec), int(bool(count))), "render_tiles")
         return rgb, lk.value, pa.value, sec.value
 
     def woodcock(self, tf, sigma_maj, origin, direction, t0, t1, seed, n):

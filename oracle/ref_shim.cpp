@@ -282,16 +282,69 @@ int ref_render(void* h, double tf_lo, double tf_hi, const float* rgba, int n_ent
     });
 }
 
-/// Tile-subset render with the reference's per-pixel body (render.hpp:295-310)
-/// over macrocells cached by ref_macrocells: only 16x16 tiles t with
-/// t % tile_stride == tile_phase are traced (bounded CPU baseline samples).
-/// Pixels outside the subset are left untouched. lookups_out counts Field
-/// reads (8 per trilinear sample). threads = 0 uses all cores.
+} // extern "C"
+
+/// Tile-subset render with the reference's per-pixel body (render.hpp:295-310) over macrocells
+/// cached by ref_macrocells: only 16x16 tiles t with t % tile_stride == tile_phase are traced
+/// (bounded CPU baseline samples). Pixels outside the subset are left untouched. With count != 0
+/// every Field read goes through CountingField (8 per trilinear sample) and lookups_out gets the
+/// total; with count == 0 the stock GridField (render.hpp:85-93) is used and lookups_out is 0, so a
+/// timed baseline carries no instrumentation. threads = 0 uses all cores.
+namespace {
+template <typename MakeField>
+void render_tile_subset(RefGrid* rg, const TransferFunction& tf, const Camera& cam, const RenderSettings& rs,
+                        int w, int hgt, int spp, uint64_t seed, int threads, int tile_stride, int tile_phase,
+                        float* rgb, uint64_t* paths_out, double* seconds, MakeField make_field)
+{
+    const MacrocellGrid& mc = *rg->mc;
+    constexpr int tile = 16;
+    int tiles_x = (w + tile - 1) / tile, tiles_y = (hgt + tile - 1) / tile;
+    std::vector<int64_t> subset;
+    for (int64_t t = 0; t < int64_t(tiles_x) * tiles_y; ++t)
+        if (t % tile_stride == tile_phase)
+            subset.push_back(t);
+    std::atomic<uint64_t> paths{0};
+    auto t0 = std::chrono::steady_clock::now();
+    parallel_for(
+        int64_t(subset.size()),
+        [&](int64_t k) {
+            auto local = make_field(k); // fresh Field (and Accessor) per tile, like render.hpp:292
+            int64_t t = subset[size_t(k)];
+            int tx = int(t % tiles_x) * tile, ty = int(t / tiles_x) * tile;
+            uint64_t np = 0;
+            for (int y = ty; y < std::min(ty + tile, hgt); ++y)
+                for (int x = tx; x < std::min(tx + tile, w); ++x) {
+                    Vec3d accum{0, 0, 0};
+                    for (int s = 0; s < spp; ++s) {
+                        Rng rng = Rng::for_pixel_sample(seed, x, y, s);
+                        double jx = rng.uniform();
+                        double jy = rng.uniform();
+                        Ray ray = detail::camera_ray(cam, x + jx, y + jy);
+                        Vec3f c = trace_path(local, mc, tf, ray, rs, rng);
+                        accum += Vec3d{double(c.x), double(c.y), double(c.z)};
+                        ++np;
+                    }
+                    accum /= double(spp);
+                    size_t o = (size_t(y) * size_t(w) + size_t(x)) * 3;
+                    rgb[o] = float(accum.x);
+                    rgb[o + 1] = float(accum.y);
+                    rgb[o + 2] = float(accum.z);
+                }
+            paths += np;
+        },
+        threads);
+    auto t1 = std::chrono::steady_clock::now();
+    *paths_out = paths.load();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
+}
+} // namespace
+
+extern "C" {
 int ref_render_tiles(void* h, double tf_lo, double tf_hi, const float* rgba, int n_entries,
                      double scale, const double* cam9, double fov, int w, int hgt, int spp,
                      int max_bounces, int rr_start, uint64_t seed, const float* ambient,
                      int threads, int tile_stride, int tile_phase, float* rgb,
-                     uint64_t* lookups_out, uint64_t* paths_out, double* seconds)
+                     uint64_t* lookups_out, uint64_t* paths_out, double* seconds, int count)
 {
     return guarded([&] {
         auto* rg = static_cast<RefGrid*>(h);
@@ -301,51 +354,18 @@ int ref_render_tiles(void* h, double tf_lo, double tf_hi, const float* rgba, int
         Camera cam = make_cam(cam9, fov, w, hgt);
         float bg[3] = {0, 0, 0};
         RenderSettings rs = make_rs(spp, max_bounces, rr_start, seed, 0, 0.5, ambient, bg, threads);
-        const MacrocellGrid& mc = *rg->mc;
-        constexpr int tile = 16;
-        int tiles_x = (w + tile - 1) / tile, tiles_y = (hgt + tile - 1) / tile;
-        std::vector<int64_t> subset;
-        for (int64_t t = 0; t < int64_t(tiles_x) * tiles_y; ++t)
-            if (t % tile_stride == tile_phase)
-                subset.push_back(t);
-        std::vector<std::uint64_t> counts(subset.size(), 0);
-        std::atomic<uint64_t> paths{0};
-        auto t0 = std::chrono::steady_clock::now();
-        parallel_for(
-            int64_t(subset.size()),
-            [&](int64_t k) {
-                CountingField local(rg->grid, &counts[size_t(k)]);
-                int64_t t = subset[size_t(k)];
-                int tx = int(t % tiles_x) * tile, ty = int(t / tiles_x) * tile;
-                uint64_t np = 0;
-                for (int y = ty; y < std::min(ty + tile, hgt); ++y)
-                    for (int x = tx; x < std::min(tx + tile, w); ++x) {
-                        Vec3d accum{0, 0, 0};
-                        for (int s = 0; s < spp; ++s) {
-                            Rng rng = Rng::for_pixel_sample(seed, x, y, s);
-                            double jx = rng.uniform();
-                            double jy = rng.uniform();
-                            Ray ray = detail::camera_ray(cam, x + jx, y + jy);
-                            Vec3f c = trace_path(local, mc, tf, ray, rs, rng);
-                            accum += Vec3d{double(c.x), double(c.y), double(c.z)};
-                            ++np;
-                        }
-                        accum /= double(spp);
-                        size_t o = (size_t(y) * size_t(w) + size_t(x)) * 3;
-                        rgb[o] = float(accum.x);
-                        rgb[o + 1] = float(accum.y);
-                        rgb[o + 2] = float(accum.z);
-                    }
-                paths += np;
-            },
-            threads);
-        auto t1 = std::chrono::steady_clock::now();
-        uint64_t total = 0;
-        for (auto c : counts)
-            total += c;
-        *lookups_out = total;
-        *paths_out = paths.load();
-        *seconds = std::chrono::duration<double>(t1 - t0).count();
+        *lookups_out = 0;
+        if (count) {
+            int tiles_x = (w + 15) / 16, tiles_y = (hgt + 15) / 16;
+            std::vector<std::uint64_t> counts(size_t(tiles_x) * size_t(tiles_y), 0);
+            render_tile_subset(rg, tf, cam, rs, w, hgt, spp, seed, threads, tile_stride, tile_phase, rgb, paths_out,
+                               seconds, [&](int64_t k) { return CountingField(rg->grid, &counts[size_t(k)]); });
+            for (auto c : counts)
+                *lookups_out += c;
+        } else {
+            render_tile_subset(rg, tf, cam, rs, w, hgt, spp, seed, threads, tile_stride, tile_phase, rgb, paths_out,
+                               seconds, [&](int64_t) { return GridField(rg->grid); });
+        }
     });
 }
 

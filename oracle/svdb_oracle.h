@@ -81,6 +81,13 @@ float so_decode(int codec, int code, float lo, float scale);
 uint64_t so_mix64(uint64_t x);
 void so_rng_uniforms(uint64_t seed, int px, int py, int s, size_t n, double* out);
 
+/* Synthetic volumes (synth_oracle.c), bit-identical to svdbgpu_synth: dense f32, x fastest. */
+int so_synth(int kind, const int32_t dims[3], uint64_t seed, int threads, float* out);
+/* Sparse field (kind 3) size calibration: per-8^3-block max of the pre-threshold density, and the
+ * threshold used at a given max dimension. */
+int so_sparse_block_max(const int32_t dims[3], uint64_t seed, int threads, double* block_max);
+double so_sparse_threshold(int dim_max);
+
 void so_free(void* p);
 
 #ifdef __cplusplus

@@ -25,7 +25,7 @@ class Settings(C.Structure):
                 ("ambient", C.c_float * 3), ("background", C.c_float * 3), ("ea_step", C.c_double),
                 ("ea_min_transmittance", C.c_double), ("tile_rank", C.c_int32),
                 ("tile_nranks", C.c_int32), ("kernel", C.c_int32), ("majorant_cell", C.c_int32),
-                ("precision", C.c_int32), ("reserved", C.c_int32 * 1)]
+                ("precision", C.c_int32), ("hdda", C.c_int32)]
 
 
 class Stats(C.Structure):

@@ -231,13 +231,16 @@ class RenderSettings:
     # (FP64 ray / DDA / distances, FP32 step log, sampler, TF, throughput) and 1 = all FP32, both
     # matching the FP64 image within a tolerance at matched streams
     precision: int = 0
+    # 1: hierarchical empty-space skipping over the node tree (lower-node level, then the majorant
+    # grid); statistically equal to the flat DDA, different streams
+    hdda: int = 0
 
     def _c(self, tile_rank: int = 0, tile_nranks: int = 1) -> N.Settings:
         return N.Settings(self.spp, self.max_bounces, self.rr_start_bounce, self.seed, int(self.mode),
                           self.iso_value, (C.c_float * 3)(*self.ambient_radiance),
                           (C.c_float * 3)(*self.background_color), self.ea_step,
                           self.ea_min_transmittance, tile_rank, tile_nranks, self.kernel,
-                          self.majorant_cell, self.precision, (C.c_int32 * 1)())
+                          self.majorant_cell, self.precision, int(self.hdda))
 
 
 @dataclass
@@ -368,6 +371,12 @@ def render_device(grid: DeviceGrid, tf: TransferFunction, cam: Camera, settings:
                                          C.c_void_p(out_ptr), int(packed), C.c_void_p(stream_ptr),
                                          C.byref(st)))
     return _stats_dict(st)
+
+
+def sample_device(grid: DeviceGrid, xyz_ptr: int, n: int, mode: int, out_ptr: int, stream_ptr: int = 0):
+    """K2 on device buffers: n positions (3 x f64 each) -> n floats (mode 0 nearest, 1 trilinear)."""
+    _check(N.lib().svdbgpu_sample_device(grid.handle, C.c_void_p(xyz_ptr), n, mode, C.c_void_p(out_ptr),
+                                         C.c_void_p(stream_ptr)))
 
 
 def tiles_for_rank(width: int, height: int, rank: int, nranks: int) -> int:

@@ -564,6 +564,27 @@ struct Octave {
     }
 };
 
+// Sparse-field (C4) threshold on d = 0.5 + 0.5 fBm per volume size (max dimension): 35% of the 8^3
+// leaf blocks hold a voxel above it. Calibrated at seed 4 from the exact per-block
+// maxima of d (tools/calibrate_sparse.py: 65th percentile); log2-linear between calibrated sizes.
+double sparse_threshold(int dim_max)
+{
+    static const int sz[] = {64, 128, 256, 512, 1024, 2048, 4096};
+    static const double th[] = {0.7263, 0.6573, 0.6089, 0.5796, 0.5630, 0.5540, 0.5494};
+    const int n = int(sizeof(sz) / sizeof(sz[0]));
+    if (dim_max <= sz[0])
+        return th[0];
+    for (int i = 1; i < n; ++i) {
+        if (dim_max == sz[i])
+            return th[i];
+        if (dim_max < sz[i]) {
+            double a = std::log2(double(sz[i - 1])), b = std::log2(double(sz[i])), x = std::log2(double(dim_max));
+            return th[i - 1] + (th[i] - th[i - 1]) * ((x - a) / (b - a));
+        }
+    }
+    return th[n - 1];
+}
+
 inline float quantise_u8(double v)
 {
     double c = std::clamp(v, 0.0, 1.0);
@@ -586,6 +607,7 @@ int synth(int kind, const int32_t dims[3], uint64_t seed, int threads, float* ou
         oct.emplace_back(base_cells << o, dmax, seed * 1315423911ull + uint64_t(o) + 1);
     const double cx = 0.5 * (dims[0] - 1), cy = 0.5 * (dims[1] - 1), cz = 0.5 * (dims[2] - 1);
     const double pi = 3.14159265358979323846;
+    const double sparse_th = sparse_threshold(dmax);
     parallel_for(rows, threads, [&](int64_t b, int64_t e, int) {
         std::vector<double> lrow;
         std::vector<const double*> rp(static_cast<size_t>(octaves));
@@ -633,9 +655,9 @@ int synth(int kind, const int32_t dims[3], uint64_t seed, int threads, float* ou
                     double t = 1.0 - f;
                     row[x] = float(std::clamp(t * t * t, 0.0, 1.0));
                 } else {
-                    // sparse field: thresholded fBm, background exactly 0
+                    // sparse field: thresholded fBm, background exactly 0, 35% of the leaf blocks
                     double d = 0.5 + 0.5 * f;
-                    row[x] = float(std::clamp((d - 0.60) * 4.0, 0.0, 1.0));
+                    row[x] = float(std::clamp((d - sparse_th) * 4.0, 0.0, 1.0));
                 }
             }
         }

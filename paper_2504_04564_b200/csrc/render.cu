@@ -1054,6 +1054,8 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         return fail_code(SVDBGPU_E_INVALID_ARG, "ea_step must be positive");
     if (st->precision < SVDBGPU_PRECISION_FP64 || st->precision > SVDBGPU_PRECISION_MIXED)
         return fail_code(SVDBGPU_E_INVALID_ARG, "unknown precision");
+    if (st->hdda)
+        return fail_code(SVDBGPU_E_UNSUPPORTED, "hierarchical DDA is not built in this library");
     const bool fp32 = st->precision != SVDBGPU_PRECISION_FP64;
     if (fp32 && (st->kernel == SVDBGPU_KERNEL_PER_PIXEL ||
                  (st->mode != SVDBGPU_MODE_PATHTRACE && st->mode != SVDBGPU_MODE_RATIO)))

@@ -68,3 +68,47 @@ def test_tile_layout_matches_native_partition():
     m = D.max_tiles(100, 37, n)
     allp = np.concatenate([D.pack_tiles(rgb, r, n, pad_to=m) for r in range(n)])
     assert np.array_equal(D.unpack_tiles(allp, n, m, 100, 37), rgb)
+
+
+def _bench(*argv, env=None):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        e.pop(k, None)
+    e.update(env or {})
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), *argv], capture_output=True, text=True,
+                       env=e, timeout=600)
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    return p.returncode, (json.loads(lines[-1]) if lines else None), p.stderr
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_bench_gpus_flag_spawns_ranks(n):
+    # `bench.py --gpus N` without a launcher re-runs itself under torch.distributed.run with N ranks;
+    # the CPU check drives the same rank wiring, encode-once sharing and product gather over gloo
+    rc, line, err = _bench("--gpus", str(n), "--cpu-check")
+    assert rc == 0, err[-2000:]
+    assert line["world"] == n and line["n_gpus"] == n and line["backend"] == "gloo"
+    assert line["bit_identical"]
+
+
+def test_bench_rejects_gpus_world_mismatch():
+    rc, line, err = _bench("--gpus", "2", "--cpu-check", env={"WORLD_SIZE": "1", "RANK": "0"})
+    assert rc == 2 and line is None and "WORLD_SIZE" in err
+
+
+def test_reference_arm_never_loads_the_product_library():
+    # --impl reference builds its input with the oracle's synth + the reference's compress and times
+    # the stock render body: libsvdbgpu.so must not be mapped (perf anchor voided)
+    from oracle.oracle import have_reference
+    if not have_reference():
+        pytest.skip("oracle/_ref not built")
+    rc, line, err = _bench("--impl", "reference", "--config", "C2", "--scale", "4", "--width", "64",
+                           "--height", "48", "--steps", "1", "--warmup", "0")
+    assert rc == 0, err[-2000:]
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert not any("libsvdbgpu" in p for p in line["native_so_loaded"])
+    assert any("libsvdbref" in p for p in line["native_so_loaded"])
