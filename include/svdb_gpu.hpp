@@ -126,6 +126,7 @@ struct RenderSettings {
     int tile_rank = 0, tile_nranks = 1;
     int majorant_cell = 0; // 0/32 reference macrocells; 8 / 128 node-majorant grids
     int precision = 0;     // SVDBGPU_PRECISION_FP64 (bit parity) / SVDBGPU_PRECISION_FP32
+    int hdda = 0;          // 1: hierarchical empty-space skipping over the node tree
 
     svdbgpu_settings c() const
     {
@@ -146,6 +147,7 @@ struct RenderSettings {
         s.tile_nranks = tile_nranks;
         s.majorant_cell = majorant_cell;
         s.precision = precision;
+        s.hdda = hdda;
         return s;
     }
 };
@@ -255,6 +257,26 @@ inline Image render(Grid& g, const TransferFunction& tf, const Camera& cam, cons
     svdbgpu_camera c = cam.c();
     svdbgpu_settings s = rs.c();
     check(svdbgpu_render(g.handle(), &t, &c, &s, img.pixels[0].data(), &img.stats));
+    return img;
+}
+
+/// render() over several devices from one process: grids[k] holds the same SVDB on device k's id;
+/// interleaved 16x16 tiles per device, one NCCL gather, the frame bit-identical to render()
+/// (svdbgpu_render_multi). gather_ms (optional) receives the gather's device time.
+inline Image render(const std::vector<Grid*>& grids, const TransferFunction& tf, const Camera& cam,
+                    const RenderSettings& rs, double* gather_ms = nullptr)
+{
+    Image img;
+    img.width = cam.width;
+    img.height = cam.height;
+    img.pixels.assign(size_t(cam.width) * size_t(cam.height), Vec3f{0, 0, 0});
+    std::vector<svdbgpu_grid*> h;
+    for (Grid* g : grids)
+        h.push_back(g ? g->handle() : nullptr);
+    svdbgpu_tf t = tf.c();
+    svdbgpu_camera c = cam.c();
+    svdbgpu_settings s = rs.c();
+    check(svdbgpu_render_multi(h.data(), int32_t(h.size()), &t, &c, &s, img.pixels[0].data(), &img.stats, gather_ms));
     return img;
 }
 

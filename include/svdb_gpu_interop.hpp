@@ -246,6 +246,35 @@ inline svdb::Image render(const svdb::FrozenGrid& grid, const svdb::TransferFunc
     throw svdb::Error(svdb::Errc::io_error, "unreachable");
 }
 
+/// Drop-in for svdb::render over several GPUs of this process (the reference's render_field tile
+/// parallel_for, render.hpp:289-313, spread over devices; SURVEY.md §8b "ndev, devs"). The grid is
+/// replicated on every listed device (cached per device) and the frame is bit-identical to
+/// svdb::gpu::render on one device.
+inline svdb::Image render(const svdb::FrozenGrid& grid, const svdb::TransferFunction& tf, const svdb::Camera& cam,
+                          const svdb::RenderSettings& settings, const std::vector<int>& devices,
+                          Codec codec = Codec::f32)
+{
+    try {
+        std::vector<std::shared_ptr<Grid>> held;
+        std::vector<Grid*> gs;
+        for (int d : devices) {
+            held.push_back(GridCache::get(grid, codec, d));
+            gs.push_back(held.back().get());
+        }
+        Image img = render(gs, convert(tf), convert(cam), convert(settings));
+        svdb::Image out;
+        out.width = img.width;
+        out.height = img.height;
+        out.pixels.resize(img.pixels.size());
+        for (size_t i = 0; i < img.pixels.size(); ++i)
+            out.pixels[i] = svdb::Vec3f{img.pixels[i][0], img.pixels[i][1], img.pixels[i][2]};
+        return out;
+    } catch (const Error& e) {
+        rethrow_as_svdb(e);
+    }
+    throw svdb::Error(svdb::Errc::io_error, "unreachable");
+}
+
 /// Drop-in for svdb::sample(const Accessor&, p, mode) (sample.hpp:97) over a device grid.
 inline float sample(const svdb::FrozenGrid& grid, const svdb::Vec3d& p, svdb::SampleMode mode)
 {

@@ -10,6 +10,8 @@
  *   svdbgpu_gradient        <- gradient(Accessor,p)      sample.hpp:81-95, 102-105
  *   svdbgpu_macrocells      <- build_macrocells()+update_majorants() macrocell.hpp:74-116
  *   svdbgpu_render          <- render(grid,tf,cam,rs)    render.hpp:319-325 (render_field 276-315)
+ *   svdbgpu_render_multi    <- render() with render_field's tile parallel_for (render.hpp:289-313)
+ *                              spread over devices, one NCCL gather (SURVEY.md §8b ndev/devs, §8e)
  *   svdbgpu_compress        <- compress(volume,params)   compress.hpp:221-283 (host encoder)
  *   svdbgpu_quantise        <- serialize_frozen()        io.hpp:121-175 (+ quantised leaf section, new)
  *
@@ -39,7 +41,8 @@ enum {
     SVDBGPU_E_INVALID_ARG = 65, /* null pointer / bad enum / size */
     SVDBGPU_E_NO_DEVICE = 66,   /* no CUDA device visible: there is NO CPU fallback */
     SVDBGPU_E_OOM = 67,         /* device allocation failed */
-    SVDBGPU_E_UNSUPPORTED = 68
+    SVDBGPU_E_UNSUPPORTED = 68,
+    SVDBGPU_E_NCCL = 69         /* NCCL missing or a collective failed (multi-device render) */
 };
 
 /* Leaf codecs of the device layout. */
@@ -176,6 +179,19 @@ int svdbgpu_render(svdbgpu_grid* g, const svdbgpu_tf* tf, const svdbgpu_camera* 
 int svdbgpu_render_device(svdbgpu_grid* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam,
                           const svdbgpu_settings* s, float* d_out, int32_t packed, void* stream,
                           svdbgpu_stats* stats);
+/* Multi-device render from one process: grids[k] holds the same SVDB on a
+ * distinct device (svdbgpu_grid_create with that device id). Device k renders the interleaved
+ * 16x16 tiles t with t % ndev == k into a packed buffer; ONE NCCL gather (grouped ncclSend/ncclRecv
+ * over NVLink/NVSwitch) brings them to grids[0]'s device, which un-interleaves them; rgb_out is the
+ * full host image W*H*3 as svdbgpu_render writes it, bit-identical for any ndev. settings->tile_*
+ * must be 0/1 (the call does the split). stats: summed paths / samples / lookups / launches, max
+ * render_ms and macrocell_ms over devices; *gather_ms (optional) = the gather's device time. NCCL
+ * (libnccl.so.2) is loaded at first use; ndev > 1 without it fails with SVDBGPU_E_NCCL. */
+int svdbgpu_render_multi(svdbgpu_grid* const* grids, int32_t ndev, const svdbgpu_tf* tf,
+                         const svdbgpu_camera* cam, const svdbgpu_settings* s, float* rgb_out,
+                         svdbgpu_stats* stats, double* gather_ms);
+/* Version of the NCCL the multi-device render uses (ncclGetVersion code, e.g. 22803). */
+int svdbgpu_nccl_version(int32_t* out);
 /* Tiles owned by rank r of n for a W x H image. */
 int64_t svdbgpu_tiles_for_rank(int32_t width, int32_t height, int32_t rank, int32_t nranks);
 /* Un-interleave nranks packed buffers (each max_tiles*768 floats, back to back) into d_rgb. */

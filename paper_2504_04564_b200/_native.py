@@ -69,6 +69,9 @@ SIGNATURES = {
                                  C.POINTER(Stats)]),
     "svdbgpu_render_device": (C.c_int, [P, C.POINTER(TF), C.POINTER(Camera), C.POINTER(Settings), P,
                                         C.c_int32, P, C.POINTER(Stats)]),
+    "svdbgpu_render_multi": (C.c_int, [P, C.c_int32, C.POINTER(TF), C.POINTER(Camera), C.POINTER(Settings), P,
+                                       C.POINTER(Stats), C.POINTER(C.c_double)]),
+    "svdbgpu_nccl_version": (C.c_int, [C.POINTER(C.c_int32)]),
     "svdbgpu_tiles_for_rank": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "svdbgpu_unpack_tiles_device": (C.c_int, [P, C.c_int32, C.c_int64, C.c_int32, C.c_int32, P, P]),
     "svdbgpu_compress": (C.c_int, [P, C.POINTER(C.c_int32), C.c_int32, C.c_double, C.c_int32,

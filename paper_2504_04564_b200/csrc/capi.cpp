@@ -54,10 +54,6 @@ int fail_code(int code, const std::string& msg)
 
 using namespace svdbgpu;
 
-struct svdbgpu_grid {
-    std::unique_ptr<GridImpl> impl;
-};
-
 namespace {
 
 template <typename F>

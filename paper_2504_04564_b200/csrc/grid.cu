@@ -388,6 +388,7 @@ GridImpl::~GridImpl()
     cudaFree(d_dir);
     cudaFree(d_tf);
     cudaFree(d_img);
+    cudaFree(d_gather);
     cudaFree(d_sbuf);
     cudaFree(d_counters);
     cudaFree(d_scratch);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -53,6 +54,8 @@ struct GridImpl {
     float4* d_tf = nullptr;
     int tf_cap = 0;
     float* d_img = nullptr;
+    float* d_gather = nullptr; // multi-device render: packed tiles of every device (first device only)
+    size_t gather_cap = 0;
     float* d_sbuf = nullptr; // per-sample results of sample-chunked renders
     size_t sbuf_cap = 0;
     size_t img_cap = 0;
@@ -83,3 +86,8 @@ int unpack_tiles(const float* d_packed, int nranks, int64_t max_tiles, int w, in
 int64_t tiles_for_rank(int w, int h, int rank, int nranks);
 
 } // namespace svdbgpu
+
+// The opaque handle of the C-ABI (include/svdbgpu.h).
+struct svdbgpu_grid {
+    std::unique_ptr<svdbgpu::GridImpl> impl;
+};

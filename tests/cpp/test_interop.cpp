@@ -78,6 +78,22 @@ int main()
         for (size_t i = 0; i < wi.pixels.size(); ++i)
             si += (std::memcmp(&wi.pixels[i], &gi.pixels[i], sizeof(Vec3f)) == 0);
         report("iso_drop_in", si >= wi.pixels.size() * 99 / 100);
+        // multi-device drop-in (svdbgpu_render_multi) over the devices visible here: the same frame
+        rs.mode = RenderMode::pathtrace;
+        rs.spp = 4;
+        int32_t ndev = 0;
+        svdbgpu_device_count(&ndev);
+        std::vector<int> devs;
+        for (int d = 0; d < ndev && d < 8; ++d)
+            devs.push_back(d);
+        Image one = gpu::render(grid, tf, cam, rs);
+        Image many = gpu::render(grid, tf, cam, rs, devs);
+        bool eq = one.pixels.size() == many.pixels.size();
+        for (size_t i = 0; eq && i < one.pixels.size(); ++i)
+            eq = std::memcmp(&one.pixels[i], &many.pixels[i], sizeof(Vec3f)) == 0;
+        char mb[48];
+        std::snprintf(mb, sizeof mb, "%zu device(s)", devs.size());
+        report("render_multi_device_drop_in", eq && !devs.empty(), mb);
     }
 
     // 3. sampler drop-in: bit-exact against sample(Accessor) (sample.hpp:97)

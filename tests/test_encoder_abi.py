@@ -87,6 +87,21 @@ def test_host_entry_points_need_no_gpu():
     assert v.shape == (8, 8, 8) and 0.0 <= v.min() and v.max() <= 1.0
 
 
+def test_nccl_loads_for_the_multi_device_render():
+    # svdbgpu_render_multi resolves NCCL at first use (no link-time dependency); the library found here
+    # is the one the NCCL gather would run on
+    v = P.nccl_version()
+    assert v >= 22700, v
+
+
+def test_render_multi_validates_arguments_without_a_gpu():
+    cam = P.Camera(width=16, height=16)
+    tf = P.TransferFunction(0.0, 1.0, [[0, 0, 0, 0], [1, 1, 1, 1]])
+    with pytest.raises(P.Error) as e:
+        P.render_multi([], tf, cam, P.RenderSettings())
+    assert e.value.status == P.api.E_INVALID_ARG
+
+
 def test_device_calls_fail_loudly_without_gpu():
     if P.device_count() > 0:
         pytest.skip("a GPU is visible")

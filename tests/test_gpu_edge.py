@@ -205,3 +205,22 @@ def test_rank_with_no_tiles_succeeds(gpu, ref):
         assert img.stats["paths"] == 0
     with pytest.raises(P.Error):
         P.render(g, TF, cam, st, tile_rank=4, tile_nranks=4)
+
+
+def test_render_multi_one_device_matches_render(gpu, ref):
+    # the single-process multi-device entry point (svdbgpu_render_multi) on the one GPU here: device
+    # split bookkeeping, packed output, k_unpack and the host copy give the render() frame bit for bit
+    svdb = _tile_grid(ref, dims=(48, 40, 36), background=0.2, seed=29)
+    g = P.DeviceGrid(svdb, P.Codec.f32, device=0)
+    cam = P.Camera(position=(23.5, 70.0, -60.0), look_at=(23.5, 19.5, 17.5), width=53, height=35)
+    for st in (P.RenderSettings(spp=4, seed=5, max_bounces=8), P.RenderSettings(spp=36, seed=6),
+               P.RenderSettings(spp=3, seed=2, mode=P.RenderMode.ratio)):
+        a = P.render(g, TF, cam, st)
+        b = P.render_multi([g], TF, cam, st)
+        assert np.array_equal(a.pixels.view(np.uint32), b.pixels.view(np.uint32))
+        assert b.stats["paths"] == a.stats["paths"] and b.stats["gather_ms"] == 0.0
+    want = ref.open(svdb).render(TF, cam, P.RenderSettings(spp=4, seed=5, max_bounces=8))
+    _check(P.render_multi([g], TF, cam, P.RenderSettings(spp=4, seed=5, max_bounces=8)).pixels, want)
+    with pytest.raises(P.Error) as e:  # one grid per device
+        P.render_multi([g, g], TF, cam, P.RenderSettings(spp=1))
+    assert e.value.status == P.api.E_INVALID_ARG
