@@ -50,7 +50,7 @@ class _Settings(C.Structure):
                 ("ambient", C.c_float * 3), ("background", C.c_float * 3),
                 ("ea_step", C.c_double), ("ea_min_transmittance", C.c_double),
                 ("tile_rank", C.c_int), ("tile_nranks", C.c_int), ("threads", C.c_int),
-                ("majorant_cell", C.c_int)]
+                ("majorant_cell", C.c_int), ("hdda", C.c_int)]
 
 
 def _take_bytes(ptr, n: int) -> bytes:
@@ -219,7 +219,8 @@ class OracleGrid:
                       (C.c_float * 3)(*settings.background_color),
                       getattr(settings, "ea_step", 0.5),
                       getattr(settings, "ea_min_transmittance", 1e-4),
-                      tile_rank, tile_nranks, threads, getattr(settings, "majorant_cell", 0))
+                      tile_rank, tile_nranks, threads, getattr(settings, "majorant_cell", 0),
+                      int(getattr(settings, "hdda", 0)))
         if rgb is None:
             rgb = np.zeros((cam.height, cam.width, 3), dtype=np.float32)
         lk = C.c_uint64()

@@ -301,6 +301,11 @@ typedef struct {
                  leaf/lower-node majorant grids (north-star node-majorant mode) */
     float *cmin, *cmax, *maj;
     uint8_t* empty;
+    /* hierarchical DDA (NEW, north-star "empty-space skipping is a hierarchical DDA over the node
+       tree"): coarse cells = 128^3 lower-node regions, cdraw[c] = some majorant-grid cell inside has
+       a positive float majorant; NULL when the flat DDA is used */
+    int ccells[3];
+    uint8_t* cdraw;
 } mc_t;
 
 static inline int cell_count_axis(int d, int cd) { int n = (d - 1 + cd - 1) / cd; return n < 1 ? 1 : n; }
@@ -338,7 +343,24 @@ static void mc_build(const so_grid* g, const so_tf* tf, int cd, mc_t* mc)
     }
 }
 
-static void mc_free(mc_t* mc) { free(mc->cmin); free(mc->cmax); free(mc->maj); free(mc->empty); }
+static void mc_free(mc_t* mc) { free(mc->cmin); free(mc->cmax); free(mc->maj); free(mc->empty); free(mc->cdraw); }
+
+#define COARSE_CELL 128
+/* coarse flags of the hierarchical DDA over the majorant grid (cell must divide 128) */
+static void mc_build_coarse(mc_t* mc)
+{
+    const int R = COARSE_CELL / mc->cell;
+    for (int a = 0; a < 3; ++a) mc->ccells[a] = cell_count_axis(mc->dims[a], COARSE_CELL);
+    size_t nc = (size_t)mc->ccells[0] * mc->ccells[1] * mc->ccells[2];
+    mc->cdraw = (uint8_t*)calloc(nc ? nc : 1, 1);
+    for (int z = 0; z < mc->cells[2]; ++z)
+        for (int y = 0; y < mc->cells[1]; ++y)
+            for (int x = 0; x < mc->cells[0]; ++x) {
+                size_t i = (size_t)x + (size_t)mc->cells[0] * ((size_t)y + (size_t)mc->cells[1] * (size_t)z);
+                if (mc->maj[i] > 0.0f)
+                    mc->cdraw[(size_t)(x / R) + (size_t)mc->ccells[0] * ((size_t)(y / R) + (size_t)mc->ccells[1] * (size_t)(z / R))] = 1;
+            }
+}
 
 static inline size_t mc_index(const mc_t* mc, const int c[3])
 {
@@ -350,6 +372,7 @@ int so_macrocells(const so_grid* g, const so_tf* tf, int* cells3, float* cmin, f
 {
     mc_t mc;
     mc_build(g, tf, 32, &mc);
+    mc.cdraw = NULL;
     memcpy(cells3, mc.cells, 12);
     size_t nc = (size_t)mc.cells[0] * mc.cells[1] * mc.cells[2];
     if (cmin && nc <= cap) {
@@ -429,16 +452,17 @@ typedef struct {
     int done;
 } dda_t;
 
-static int dda_init(const mc_t* mc, const ray_t* r, double t0, double t1, dda_t* s)
+static int dda_init_cells(const int dims[3], const int cells[3], int cell, const ray_t* r, double t0, double t1,
+                          dda_t* s)
 {
     double lo[3] = {0, 0, 0};
-    double hi[3] = {(double)(mc->dims[0] - 1), (double)(mc->dims[1] - 1), (double)(mc->dims[2] - 1)};
+    double hi[3] = {(double)(dims[0] - 1), (double)(dims[1] - 1), (double)(dims[2] - 1)};
     if (!clip_ray_box(r, lo, hi, &t0, &t1)) return 0;
     if (!(t0 <= t1)) return 0;
-    double e[3], cs = (double)mc->cell;
+    double e[3], cs = (double)cell;
     ray_at(r, t0, e);
     for (int a = 0; a < 3; ++a) {
-        s->c[a] = (int)dclamp(floor(e[a] / cs), 0.0, (double)(mc->cells[a] - 1));
+        s->c[a] = (int)dclamp(floor(e[a] / cs), 0.0, (double)(cells[a] - 1));
         s->step[a] = 0;
         s->t_next[a] = INFINITY;
         s->t_delta[a] = INFINITY;
@@ -459,8 +483,13 @@ static int dda_init(const mc_t* mc, const ray_t* r, double t0, double t1, dda_t*
     return 1;
 }
 
-/* Produces the next visit (cell, ta, tb); the visitor's "continue" is implicit. */
-static int dda_next(const mc_t* mc, dda_t* s, int cell[3], double* ta, double* tb)
+static int dda_init(const mc_t* mc, const ray_t* r, double t0, double t1, dda_t* s)
+{
+    return dda_init_cells(mc->dims, mc->cells, mc->cell, r, t0, t1, s);
+}
+
+/* Produces the next visit (cell, ta, tb) over a grid of `cells`; "continue" is implicit. */
+static int dda_next_cells(const int cells[3], dda_t* s, int cell[3], double* ta, double* tb)
 {
     if (s->done) return 0;
     int axis = 0;
@@ -474,9 +503,56 @@ static int dda_next(const mc_t* mc, dda_t* s, int cell[3], double* ta, double* t
     if (t_exit >= s->t1) { s->done = 1; return 1; }
     s->t_cur = t_exit;
     s->c[axis] += s->step[axis];
-    if (s->c[axis] < 0 || s->c[axis] >= mc->cells[axis]) { s->done = 1; return 1; }
+    if (s->c[axis] < 0 || s->c[axis] >= cells[axis]) { s->done = 1; return 1; }
     s->t_next[axis] += s->t_delta[axis];
     return 1;
+}
+
+static int dda_next(const mc_t* mc, dda_t* s, int cell[3], double* ta, double* tb)
+{
+    return dda_next_cells(mc->cells, s, cell, ta, tb);
+}
+
+/* One flight's majorant-cell visits. Flat: the reference's DDA (dda.hpp:52-109) over the majorant
+ * grid. Hierarchical (mc->cdraw): a DDA over 128^3 lower-node regions skips regions without draws
+ * in one step; inside a region with draws the majorant-grid DDA restarts at the region entry
+ * (dda_init on [ta_c, tb_c]) and its visits are produced in order. */
+typedef struct {
+    const mc_t* mc;
+    const ray_t* ray;
+    dda_t coarse, fine;
+    int in_fine;
+} flight_t;
+
+static int flight_init(const mc_t* mc, const ray_t* r, flight_t* f)
+{
+    f->mc = mc;
+    f->ray = r;
+    f->in_fine = 0;
+    if (!mc->cdraw) {
+        f->in_fine = 1;
+        return dda_init(mc, r, 0.0, INFINITY, &f->fine);
+    }
+    return dda_init_cells(mc->dims, mc->ccells, COARSE_CELL, r, 0.0, INFINITY, &f->coarse);
+}
+
+static int flight_next(flight_t* f, int cell[3], double* ta, double* tb)
+{
+    const mc_t* mc = f->mc;
+    if (!mc->cdraw)
+        return dda_next(mc, &f->fine, cell, ta, tb);
+    for (;;) {
+        if (f->in_fine) {
+            if (dda_next(mc, &f->fine, cell, ta, tb)) return 1;
+            f->in_fine = 0;
+        }
+        int cc[3];
+        double a, b;
+        if (!dda_next_cells(mc->ccells, &f->coarse, cc, &a, &b)) return 0;
+        if (!mc->cdraw[(size_t)cc[0] + (size_t)mc->ccells[0] * ((size_t)cc[1] + (size_t)mc->ccells[1] * (size_t)cc[2])])
+            continue;
+        if (dda_init(mc, f->ray, a, b, &f->fine)) f->in_fine = 1;
+    }
 }
 
 /* ---- integrators: render.hpp:100-187 ---- */
@@ -509,11 +585,11 @@ static int woodcock(ctx_t* cx, double sigma_maj, const ray_t* r, double t0, doub
 /* next_event (render.hpp:137-151) */
 static int next_event(ctx_t* cx, const ray_t* r, rng_t* rng, double* t_ev, float* v_ev)
 {
-    dda_t d;
-    if (!dda_init(cx->mc, r, 0.0, INFINITY, &d)) return 0;
+    flight_t d;
+    if (!flight_init(cx->mc, r, &d)) return 0;
     int c[3];
     double ta, tb;
-    while (dda_next(cx->mc, &d, c, &ta, &tb)) {
+    while (flight_next(&d, c, &ta, &tb)) {
         size_t ci = mc_index(cx->mc, c);
         if (cx->mc->empty[ci]) continue;
         if (woodcock(cx, (double)cx->mc->maj[ci], r, ta, tb, rng, t_ev, v_ev)) return 1;
@@ -578,11 +654,11 @@ static void trace_ratio(ctx_t* cx, ray_t ray, rng_t* rng, float out[3])
         int have = 0;
         double t_ev = 0.0;
         float v_ev = 0.0f;
-        dda_t d;
-        if (dda_init(cx->mc, &ray, 0.0, INFINITY, &d)) {
+        flight_t d;
+        if (flight_init(cx->mc, &ray, &d)) {
             int c[3];
             double ta, tb;
-            while (Tr > 0.0 && dda_next(cx->mc, &d, c, &ta, &tb)) {
+            while (Tr > 0.0 && flight_next(&d, c, &ta, &tb)) {
                 size_t ci = mc_index(cx->mc, c);
                 if (cx->mc->empty[ci]) continue;
                 double sm = (double)cx->mc->maj[ci];
@@ -810,8 +886,12 @@ int so_render(const so_grid* g, const so_tf* tf, const so_camera* cam, const so_
     int cd = s->majorant_cell;
     if (cd == 0) cd = 32;
     if (cd != 8 && cd != 32 && cd != 128) return E_SIZE;
+    if (s->hdda && cd >= COARSE_CELL) return E_SIZE;
     mc_t mc;
     mc_build(g, tf, cd, &mc);
+    mc.cdraw = NULL;
+    if (s->hdda && (s->mode == SO_PATHTRACE || s->mode == SO_RATIO))
+        mc_build_coarse(&mc);
     int tiles_x = (cam->width + 15) / 16, tiles_y = (cam->height + 15) / 16;
     long total = (long)tiles_x * tiles_y;
     int nr = s->tile_nranks > 0 ? s->tile_nranks : 1;

@@ -52,6 +52,7 @@ typedef struct {
     int tile_rank, tile_nranks;  /* interleaved 16x16 tiles: t % nranks == rank */
     int threads;                 /* 0 = all cores */
     int majorant_cell;           /* 0/32 reference macrocells; 8 / 128 node-majorant grids */
+    int hdda;                    /* 1: hierarchical DDA (128^3 lower-node regions, then the majorant grid) */
 } so_settings;
 
 /* SVDB v1 container (io.hpp:22-43); returns 0 or Errc+1 (errors.hpp:11-23). */

@@ -8,6 +8,7 @@
 #include "device.cuh"
 #include "grid_impl.hpp"
 
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 #include <cmath>
@@ -389,6 +390,7 @@ GridImpl::~GridImpl()
     cudaFree(d_tf);
     cudaFree(d_img);
     cudaFree(d_gather);
+    cudaFree(d_cdraw);
     cudaFree(d_sbuf);
     cudaFree(d_counters);
     cudaFree(d_scratch);
@@ -496,6 +498,43 @@ int majorants(GridImpl* g, const DevTF& tf, cudaStream_t s, uint8_t* d_empty)
     int nc = g->cells[0] * g->cells[1] * g->cells[2];
     k_majorants<<<(nc + 255) / 256, 256, tf_smem_bytes(tf.n), s>>>(tf, g->d_tf, g->d_cmin, g->d_cmax, nc,
                                                                             g->d_maj, g->d_inv_maj, g->d_inv_maj_f, d_empty);
+    SVDB_CUDA(cudaGetLastError());
+    return 0;
+}
+
+// Hierarchical DDA (render settings.hdda): one flag per 128^3 lower-node region over the majorant
+// grid of g->cell_dim (which divides 128): set when some majorant cell inside has a positive float
+// majorant, i.e. tracking would draw there (oracle/svdb_oracle.c mc_build_coarse).
+__global__ void k_coarse_flags(const float* __restrict__ maj, int3 cells, int R, int3 cc, uint8_t* __restrict__ draw)
+{
+    const int n = cc.x * cc.y * cc.z;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int x0 = (i % cc.x) * R, y0 = ((i / cc.x) % cc.y) * R, z0 = (i / (cc.x * cc.y)) * R;
+        uint8_t any = 0;
+        for (int z = z0; z < min(z0 + R, cells.z) && !any; ++z)
+            for (int y = y0; y < min(y0 + R, cells.y) && !any; ++y)
+                for (int x = x0; x < min(x0 + R, cells.x); ++x)
+                    if (maj[x + cells.x * (y + cells.y * z)] > 0.0f) {
+                        any = 1;
+                        break;
+                    }
+        draw[i] = any;
+    }
+}
+
+int coarse_flags(GridImpl* g, const int ccells[3], cudaStream_t s)
+{
+    const size_t n = size_t(ccells[0]) * size_t(ccells[1]) * size_t(ccells[2]);
+    if (n > g->cdraw_cap || !g->d_cdraw) {
+        cudaFree(g->d_cdraw);
+        g->d_cdraw = nullptr;
+        g->cdraw_cap = 0;
+        SVDB_CUDA(cudaMalloc(&g->d_cdraw, n));
+        g->cdraw_cap = n;
+    }
+    k_coarse_flags<<<unsigned(std::min<size_t>((n + 255) / 256, 148 * 8)), 256, 0, s>>>(
+        g->d_maj, make_int3(g->cells[0], g->cells[1], g->cells[2]), 128 / g->cell_dim,
+        make_int3(ccells[0], ccells[1], ccells[2]), g->d_cdraw);
     SVDB_CUDA(cudaGetLastError());
     return 0;
 }

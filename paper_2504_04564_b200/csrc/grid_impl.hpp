@@ -51,6 +51,8 @@ struct GridImpl {
     double* d_inv_maj = nullptr; // 1.0 / double(majorant), 0 for empty cells
     float* d_inv_maj_f = nullptr; // the same in float (FP32 tracking kernel)
     bool ranges_valid = false;
+    uint8_t* d_cdraw = nullptr; // hierarchical DDA: per 128^3 region, "some majorant cell has draws"
+    size_t cdraw_cap = 0;
     float4* d_tf = nullptr;
     int tf_cap = 0;
     float* d_img = nullptr;
@@ -79,6 +81,7 @@ int read_voxels_device(const GridImpl* g, const int32_t* d_ijk, size_t n, float*
 int sample_device(const GridImpl* g, const double* d_xyz, size_t n, int mode, float* d_out, cudaStream_t s);
 int gradient_device(const GridImpl* g, const double* d_xyz, size_t n, double* d_out, cudaStream_t s);
 int majorants(GridImpl* g, const DevTF& tf, cudaStream_t s, uint8_t* d_empty = nullptr);
+int coarse_flags(GridImpl* g, const int ccells[3], cudaStream_t s);
 int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const svdbgpu_settings* st,
            float* d_out, int packed, cudaStream_t s, svdbgpu_stats* stats);
 int unpack_tiles(const float* d_packed, int nranks, int64_t max_tiles, int w, int h, float* d_rgb,

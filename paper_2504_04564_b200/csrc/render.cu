@@ -464,7 +464,8 @@ __global__ void __launch_bounds__(256) k_render(const __grid_constant__ RenderAr
 // the image is bit-identical to k_render and to the CPU oracles. Pixels are handed out in 8x4
 // blocks per warp from a global counter (lanes refill individually, so no lane idles at a pixel
 // boundary); the grid is sized to the resident CTA count.
-enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4, kPoint = 5, kScatter = 6 };
+enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4, kPoint = 5, kScatter = 6,
+             kNeedRegion = 7 }; // kNeedRegion: hierarchical DDA, next 128^3 lower-node region
 
 // The macrocell DDA of device.cuh (dda.hpp:52-109), same arithmetic, with its 23 words of
 // per-lane state in shared memory (SoA, conflict-free) instead of registers: it is touched once
@@ -578,7 +579,7 @@ constexpr int kChunkMinSpp = 16;    // one GPU: whole-pixel work items below thi
 constexpr int kSplitChunk = 4;      // max samples per work item when the frame is split over ranks
 constexpr int kSampleChunk = 16;    // max samples per work item on one GPU
 
-template <int CODEC, int MODE, bool CHUNK>
+template <int CODEC, int MODE, bool CHUNK, bool HDDA>
 __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
 {
     extern __shared__ float4 s_tf[];
@@ -615,6 +616,10 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     __shared__ int s_dda_i[7][T];
     __shared__ double s_dda_d[8][T];
     SharedDda<T> dda{&s_dda_i[0][0], &s_dda_d[0][0], tid};
+    // hierarchical DDA: the lower-node-region DDA of the flight (oracle flight_init / flight_next)
+    __shared__ int s_rdda_i[HDDA ? 7 : 1][T];
+    __shared__ double s_rdda_d[HDDA ? 8 : 1][T];
+    SharedDda<T> rdda{&s_rdda_i[0][0], &s_rdda_d[0][0], tid};
     // The step loop's live values stay in registers: t, the cell's far end tb, 1/majorant of this
     // cell and of the next one (loaded one visit ahead), the RNG state.
     double t = 0.0, tb = 0.0, inv = 0.0, inv_ahead = 0.0;
@@ -769,6 +774,14 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             Tr = 1.0;
             have = false;
         }
+        if constexpr (HDDA) {
+            if (!rdda.init(A.ccells, A.hi, ray_load(), 0.0, kInf(), 128.0, 1.0 / 128.0)) {
+                end_segment();
+                return;
+            }
+            state = kNeedRegion;
+            return;
+        }
         if (!dda.init(A.cells, A.hi, ray_load(), 0.0, kInf(), A.cell, A.icell)) {
             end_segment();
             return;
@@ -783,11 +796,35 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         // the cell lookup (independent FP64 chains interleave); the draw is consumed only if the
         // cell has draws, so the stream is unchanged
         const double lg = step_log(1.0 - rng.peek());
+        if constexpr (HDDA) {
+            if (state == kNeedRegion) { // next lower-node region; one without draws is skipped whole
+                int rc[3];
+                double ra, rb;
+                if (!rdda.next(A.ccells, rc, ra, rb)) {
+                    end_segment();
+                    return;
+                }
+                if (!__ldg(A.cdraw + (rc[0] + A.ccells[0] * (rc[1] + A.ccells[1] * rc[2]))))
+                    return;
+                if (!dda.init(A.cells, A.hi, ray_load(), ra, rb, A.cell, A.icell))
+                    return;
+                inv_ahead = __ldg(A.inv_maj + dda.index(A.cells));
+                state = kNeedCell;
+                return;
+            }
+        }
         if (state == kNeedCell) {
             int c[3];
             double ta, tbb;
-            if ((RATIO && !(Tr > 0.0)) || !dda.next(A.cells, c, ta, tbb)) {
+            if (RATIO && !(Tr > 0.0)) {
                 end_segment();
+                return;
+            }
+            if (!dda.next(A.cells, c, ta, tbb)) {
+                if constexpr (HDDA)
+                    state = kNeedRegion; // the region's majorant cells are done
+                else
+                    end_segment();
                 return;
             }
             // 1.0 / double(majorant) precomputed per cell with the same IEEE division
@@ -897,7 +934,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         // ---- phase selection: run the one phase most lanes are waiting in; ties go to the
         // gather so its memory latency is paid by as many lanes as possible at once ----
         const int nS = __popc(__ballot_sync(live, state == kPoint));
-        const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell));
+        const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell || state == kNeedRegion));
         const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter));
         const int phase = (nS > 0 && nS >= nA && nS >= nT) || (nA == 0 && nT == 0) ? 2 : (nA >= nT ? 1 : 0);
 #ifdef SVDB_PHASE_STATS
@@ -912,7 +949,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                 do_start();
         } else if (phase == 1) {
 #pragma unroll 1
-            for (int k = 0; k < kAdvIters && (state == kNeedCell || state == kInCell); ++k)
+            for (int k = 0; k < kAdvIters && (state == kNeedCell || state == kInCell || state == kNeedRegion); ++k)
                 do_advance();
         } else if (state == kPoint) {
             do_sample();
@@ -1054,8 +1091,14 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         return fail_code(SVDBGPU_E_INVALID_ARG, "ea_step must be positive");
     if (st->precision < SVDBGPU_PRECISION_FP64 || st->precision > SVDBGPU_PRECISION_MIXED)
         return fail_code(SVDBGPU_E_INVALID_ARG, "unknown precision");
-    if (st->hdda)
-        return fail_code(SVDBGPU_E_UNSUPPORTED, "hierarchical DDA is not built in this library");
+    const bool hdda = st->hdda != 0;
+    if (hdda && (st->precision != SVDBGPU_PRECISION_FP64 || st->kernel == SVDBGPU_KERNEL_PER_PIXEL ||
+                 (st->mode != SVDBGPU_MODE_PATHTRACE && st->mode != SVDBGPU_MODE_RATIO)))
+        return fail_code(SVDBGPU_E_UNSUPPORTED, "the hierarchical DDA is implemented for FP64 pathtrace / ratio "
+                                                "tracking in the path-regenerating kernel");
+    if (hdda && st->majorant_cell >= 128)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "hierarchical DDA: the majorant grid must be finer than the "
+                                                "128^3 lower-node regions (majorant_cell 8 or 32)");
     const bool fp32 = st->precision != SVDBGPU_PRECISION_FP64;
     if (fp32 && (st->kernel == SVDBGPU_KERNEL_PER_PIXEL ||
                  (st->mode != SVDBGPU_MODE_PATHTRACE && st->mode != SVDBGPU_MODE_RATIO)))
@@ -1071,6 +1114,14 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     SVDB_CUDA(cudaEventRecord(g->ev0, s));
     if (int rc = majorants(g, A.tf, s))
         return rc;
+    A.cdraw = nullptr;
+    if (hdda) {
+        for (int a = 0; a < 3; ++a)
+            A.ccells[a] = std::max(1, (g->dg.dims[a] - 1 + 127) / 128); // cell_counts_for at 128
+        if (int rc = coarse_flags(g, A.ccells, s))
+            return rc;
+        A.cdraw = g->d_cdraw;
+    }
     SVDB_CUDA(cudaEventRecord(g->ev1, s));
     SVDB_CUDA(cudaMemsetAsync(g->d_counters, 0, 128, s));
 
@@ -1148,7 +1199,8 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
 #define LAUNCH_T(C, M)                                                                         \
     {                                                                                          \
         int per_sm = 1;                                                                        \
-        auto kern = A.chunk ? k_trace<C, M, true> : k_trace<C, M, false>;                         \
+        auto kern = hdda ? (A.chunk ? k_trace<C, M, true, true> : k_trace<C, M, false, true>)    \
+                         : (A.chunk ? k_trace<C, M, true, false> : k_trace<C, M, false, false>); \
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTraceThreads, smem);       \
         long long blocks = std::min<long long>((long long)std::max(per_sm, 1) * sms, (n_units * 32 + kTraceThreads - 1) / kTraceThreads); \
         kern<<<unsigned(blocks), kTraceThreads, smem, s>>>(A, n_units);                          \
@@ -1222,7 +1274,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         stats->lookups = samples * 8;
         stats->render_ms = rms;
         stats->macrocell_ms = double(range_ms) + double(mms);
-        stats->launches = (range_ms > 0.0f ? 1u : 0u) + 1u + (ntiles > 0 ? 1u : 0u) + (A.chunk ? 1u : 0u);
+        stats->launches = (range_ms > 0.0f ? 1u : 0u) + 1u + (hdda ? 1u : 0u) + (ntiles > 0 ? 1u : 0u) + (A.chunk ? 1u : 0u);
     }
     return 0;
 }

@@ -24,6 +24,10 @@ struct RenderArgs {
     const float* inv_maj_f; // float(1 / majorant), 0 for cells without draws (FP32 tracking)
     const float* cmin;
     const float* cmax;
+    // hierarchical DDA (settings.hdda): 128^3 lower-node regions over the majorant grid; cdraw[c] != 0
+    // when some majorant cell inside region c has draws
+    int ccells[3];
+    const uint8_t* cdraw;
     int cells[3];
     double cell;  // majorant cell edge in voxels (32 = the reference's MacrocellGrid::cell_dim)
     double icell; // 1/cell, exact (cell is a power of two), so e * icell == e / cell bit for bit

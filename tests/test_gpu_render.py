@@ -215,3 +215,38 @@ def test_homogeneous_cube_matches_independent_mc(gpu, ref):
         img = P.render(g, tf, cam, P.RenderSettings(spp=256, seed=99, mode=mode))
         ours = img.pixels[..., 0].mean()
         assert abs(ours - ref_mean) < 3 * ref_se + 0.004, (mode, ours, ref_mean)
+
+
+@pytest.mark.parametrize("cell", [32, 8])
+@pytest.mark.parametrize("mode", [P.RenderMode.pathtrace, P.RenderMode.ratio])
+def test_hdda_matches_oracle_on_multi_region_grid(gpu, orc, cell, mode):
+    # hierarchical DDA (a23): 128^3 lower-node regions without draws skipped in one step, the
+    # majorant grid walked inside the others. Sparse C4 field at 256^3 (8 regions) and 512^3 (64): the
+    # GPU consumes the same streams as the oracle's flight_next, visit for visit
+    for factor, imf in ((8, 32), (4, 48)):
+        sc = S.scaled("C4", factor, spp=4, image_factor=imf, mode=mode)
+        st = P.RenderSettings(spp=4, seed=7, max_bounces=64, rr_start_bounce=3, mode=mode, majorant_cell=cell,
+                              hdda=1)
+        _, svdb, _ = scene_svdb(sc)
+        g = P.DeviceGrid(svdb, P.Codec.affine8)
+        deq, _, _ = orc.quantize(svdb, int(P.Codec.affine8))
+        og = orc.open(deq)
+        img, (want, lookups, _) = _render_pair(lambda tf, cam, s: og.render(tf, cam, s), g, sc, st)
+        same, rmse = image_parity(img.pixels, want)
+        print(f"{sc.dims[0]}^3 cell {cell} {mode.name}: identical {same:.4f} rmse {rmse:.2e}")
+        assert rmse <= RMSE_TOL and same >= 0.999
+        if mode == P.RenderMode.pathtrace:
+            assert abs(img.stats["lookups"] - lookups) <= 1e-3 * lookups
+
+
+def test_hdda_is_unbiased_and_validated(gpu):
+    sc = S.scaled("C4", 4, spp=16, image_factor=16)
+    _, svdb, _ = scene_svdb(sc)
+    g = P.DeviceGrid(svdb, P.Codec.affine8)
+    cam = sc.camera()
+    base = P.render(g, sc.tf, cam, P.RenderSettings(spp=16, seed=3, mode=P.RenderMode.ratio))
+    hier = P.render(g, sc.tf, cam, P.RenderSettings(spp=16, seed=3, mode=P.RenderMode.ratio, hdda=1))
+    assert abs(hier.pixels.mean() - base.pixels.mean()) < 3e-3
+    for bad in (dict(majorant_cell=128, hdda=1), dict(precision=2, hdda=1), dict(mode=P.RenderMode.ea, hdda=1)):
+        with pytest.raises(P.Error):
+            P.render(g, sc.tf, cam, P.RenderSettings(spp=1, **bad))

@@ -196,3 +196,33 @@ def test_ea_transmittance_is_beer_lambert(orc, ref):
     img, _, _ = og.render(tf, cam, st)
     # ray length through the box ~64 voxels; n = 128 samples of dt 0.5 (+/- one at the ends)
     assert np.all(np.abs(img[..., 0] - np.exp(-sigma * 64.0)) < 0.02)
+
+
+def test_hdda_in_one_lower_node_region_is_the_flat_dda(orc):
+    # a grid inside one 128^3 lower-node region: the coarse DDA visits that single region over the
+    # clipped segment and the majorant-grid DDA restarts at its entry -> exactly the flat traversal
+    sc = S.scaled("C3", 16, spp=4, image_factor=16)
+    _, svdb, _ = scene_svdb(sc)
+    og = orc.open(svdb)
+    cam = sc.camera()
+    for mode in (P.RenderMode.pathtrace, P.RenderMode.ratio):
+        st = P.RenderSettings(spp=4, seed=3, mode=mode)
+        a, _, _ = og.render(sc.tf, cam, st)
+        b, _, _ = og.render(sc.tf, cam, P.RenderSettings(spp=4, seed=3, mode=mode, hdda=1))
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+@pytest.mark.parametrize("mode", [P.RenderMode.pathtrace, P.RenderMode.ratio])
+def test_hdda_skips_empty_regions_without_bias(orc, mode):
+    # the sparse C4 field at 256^3 (2 x 2 x 2 lower-node regions, some without draws): skipping a
+    # region in one step changes where the majorant-grid DDA restarts, not the estimator
+    sc = S.scaled("C4", 8, spp=64, image_factor=40)
+    _, svdb, _ = scene_svdb(sc)
+    og = orc.open(svdb)
+    cam = sc.camera()
+    st = dict(spp=64, seed=11, max_bounces=64, rr_start_bounce=3, mode=mode)
+    flat, _, _ = og.render(sc.tf, cam, P.RenderSettings(**st))
+    hier, _, _ = og.render(sc.tf, cam, P.RenderSettings(**st, hdda=1))
+    assert abs(hier.mean() - flat.mean()) < 4e-3
+    with pytest.raises(RuntimeError):  # the coarse level is the lower node: majorant cells must be finer
+        og.render(sc.tf, cam, P.RenderSettings(spp=1, majorant_cell=128, hdda=1))
