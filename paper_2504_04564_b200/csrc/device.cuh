@@ -404,10 +404,10 @@ __device__ __forceinline__ double tf_max_alpha_in_range(const DevTF& tf, const f
 #ifndef SVDB_GLIBC_LOG
 #define SVDB_GLIBC_LOG 0 // 1: step lengths bit-exact to the reference; measured -5% (C3) / -7% (C4)
 #endif
-__device__ __forceinline__ double step_log(double w)
+__device__ __forceinline__ double step_log(double w, const LogTabEntry* smem_tab = nullptr)
 {
 #if SVDB_GLIBC_LOG
-    return glibc_log(w);
+    return glibc_log(w, smem_tab);
 #else
     return log(w);
 #endif

@@ -391,6 +391,7 @@ GridImpl::~GridImpl()
     cudaFree(d_img);
     cudaFree(d_gather);
     cudaFree(d_cdraw);
+    cudaFree(d_camtab);
     cudaFree(d_sbuf);
     cudaFree(d_counters);
     cudaFree(d_scratch);

@@ -60,6 +60,8 @@ struct GridImpl {
     size_t gather_cap = 0;
     float* d_sbuf = nullptr; // per-sample results of sample-chunked renders
     size_t sbuf_cap = 0;
+    double2* d_camtab = nullptr; // precomputed camera rays of sample-chunked renders
+    size_t camtab_cap = 0;
     size_t img_cap = 0;
     unsigned long long* d_counters = nullptr;
     double* d_scratch = nullptr;

@@ -112,122 +112,18 @@ inline uint32_t f32_bits(float f) { uint32_t u; std::memcpy(&u, &f, 4); return u
 
 } // namespace
 
-int compress(const float* data, const int32_t dims[3], int voxel_type, double quality, int metric,
-             int threads, std::vector<uint8_t>& out, svdbgpu_compress_report* rep)
+// Stage 3-4 of compress (compress.hpp:97-145, 237-251): brick scores against the background, the
+// total order (score desc, non-background first, index), the ceil(q * n) budget and the voxel count
+// it activates (+ the two corner voxels set_voxel adds).
+void choose_bricks(const int32_t dims[3], const float* blo, const float* bhi, float bg, int metric, double quality,
+                   std::vector<uint8_t>& chosen, uint64_t& budget_out, uint64_t& voxels_activated)
 {
-    if (!(quality >= 0.0 && quality <= 1.0))
-        return fail(Errc::invalid_quality, "quality must be in [0,1]");
-    if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
-        return fail(Errc::size_mismatch, "volume dims must be positive");
-    if (voxel_type != 0 && voxel_type != 1)
-        return fail(Errc::size_mismatch, "voxel_type must be 0 (u8) or 1 (f32)");
-    const Vol v{data, dims[0], dims[1], dims[2]};
-    const int64_t nvox = int64_t(dims[0]) * dims[1] * dims[2];
-    const int nt = resolve_threads(threads);
-    const int64_t rows = int64_t(dims[1]) * dims[2];
-
-    // 1. min / max / finiteness (volume.hpp:41-62)
-    std::vector<float> tmin(size_t(nt), std::numeric_limits<float>::infinity());
-    std::vector<float> tmax(size_t(nt), -std::numeric_limits<float>::infinity());
-    std::atomic<bool> nonfinite{false};
-    parallel_for(rows, nt, [&](int64_t b, int64_t e, int t) {
-        float mn = tmin[size_t(t)], mx = tmax[size_t(t)];
-        for (int64_t r = b; r < e; ++r) {
-            const float* row = data + size_t(r) * size_t(dims[0]);
-            for (int x = 0; x < dims[0]; ++x) {
-                float s = nz(row[x]);
-                if (!std::isfinite(s))
-                    nonfinite = true;
-                mn = std::min(mn, s);
-                mx = std::max(mx, s);
-            }
-        }
-        tmin[size_t(t)] = mn;
-        tmax[size_t(t)] = mx;
-    });
-    if (nonfinite)
-        return fail(Errc::non_finite_voxel, "volume contains NaN or Inf");
-    float vmin = std::numeric_limits<float>::infinity(), vmax = -vmin;
-    for (int t = 0; t < nt; ++t) {
-        vmin = std::min(vmin, tmin[size_t(t)]);
-        vmax = std::max(vmax, tmax[size_t(t)]);
-    }
-
-    // 2. histogram + background (volume.hpp:177-222)
-    const int bins = voxel_type == 0 ? 256 : 1024;
-    const double hlo = vmin, hhi = vmax;
-    auto bin_of = [&](double s) {
-        if (hhi <= hlo)
-            return 0;
-        int b = int(std::floor((s - hlo) / (hhi - hlo) * double(bins)));
-        return std::clamp(b, 0, bins - 1);
-    };
-    std::vector<std::vector<uint64_t>> th(size_t(nt), std::vector<uint64_t>(size_t(bins), 0));
-    parallel_for(rows, nt, [&](int64_t b, int64_t e, int t) {
-        auto& h = th[size_t(t)];
-        for (int64_t r = b; r < e; ++r) {
-            const float* row = data + size_t(r) * size_t(dims[0]);
-            for (int x = 0; x < dims[0]; ++x)
-                ++h[size_t(bin_of(nz(row[x])))];
-        }
-    });
-    std::vector<uint64_t> hist(size_t(bins), 0);
-    for (auto& h : th)
-        for (int i = 0; i < bins; ++i)
-            hist[size_t(i)] += h[size_t(i)];
-    int best_bin = 0;
-    for (int i = 1; i < bins; ++i)
-        if (hist[size_t(i)] > hist[size_t(best_bin)])
-            best_bin = i;
-    std::vector<std::unordered_map<float, uint64_t>> exact(static_cast<size_t>(nt));
-    parallel_for(rows, nt, [&](int64_t b, int64_t e, int t) {
-        auto& m = exact[size_t(t)];
-        for (int64_t r = b; r < e; ++r) {
-            const float* row = data + size_t(r) * size_t(dims[0]);
-            for (int x = 0; x < dims[0]; ++x) {
-                float s = nz(row[x]);
-                if (bin_of(s) == best_bin)
-                    ++m[s];
-            }
-        }
-    });
-    for (int t = 1; t < nt; ++t)
-        for (auto& [val, cnt] : exact[size_t(t)])
-            exact[0][val] += cnt;
-    bool have = false;
-    float bg = 0.0f;
-    uint64_t best_count = 0;
-    for (auto& [val, cnt] : exact[0])
-        if (!have || cnt > best_count || (cnt == best_count && val < bg)) {
-            have = true;
-            bg = val;
-            best_count = cnt;
-        }
-
-    // 3. brick records + total order (compress.hpp:97-145)
     const int nbx = (dims[0] + kBrick - 1) / kBrick, nby = (dims[1] + kBrick - 1) / kBrick,
               nbz = (dims[2] + kBrick - 1) / kBrick;
     const int64_t total = int64_t(nbx) * nby * nbz;
     std::vector<Brick> bricks(static_cast<size_t>(total));
-    parallel_for(total, nt, [&](int64_t b, int64_t e, int) {
-        for (int64_t i = b; i < e; ++i) {
-            int bx = int(i % nbx), by = int((i / nbx) % nby), bz = int(i / (int64_t(nbx) * nby));
-            int x0 = bx * kBrick, y0 = by * kBrick, z0 = bz * kBrick;
-            int x1 = std::min(x0 + kBrick, dims[0]), y1 = std::min(y0 + kBrick, dims[1]),
-                z1 = std::min(z0 + kBrick, dims[2]);
-            float mn = std::numeric_limits<float>::infinity(), mx = -mn;
-            for (int z = z0; z < z1; ++z)
-                for (int y = y0; y < y1; ++y) {
-                    const float* row = v.row(x0, y, z);
-                    for (int x = 0; x < x1 - x0; ++x) {
-                        float s = nz(row[x]);
-                        mn = std::min(mn, s);
-                        mx = std::max(mx, s);
-                    }
-                }
-            bricks[size_t(i)] = {mn, mx, similarity(mn, mx, bg, metric), uint64_t(i)};
-        }
-    });
+    for (int64_t i = 0; i < total; ++i)
+        bricks[size_t(i)] = {blo[i], bhi[i], similarity(blo[i], bhi[i], bg, metric), uint64_t(i)};
     std::sort(bricks.begin(), bricks.end(), [bg](const Brick& a, const Brick& b) {
         if (a.score != b.score)
             return a.score > b.score;
@@ -238,8 +134,8 @@ int compress(const float* data, const int32_t dims[3], int voxel_type, double qu
     });
     const uint64_t budget =
         std::min<uint64_t>(uint64_t(total), uint64_t(std::ceil(quality * double(total))));
-    std::vector<uint8_t> chosen(size_t(total), 0);
-    uint64_t voxels_activated = 0;
+    chosen.assign(size_t(total), 0);
+    voxels_activated = 0;
     for (uint64_t i = 0; i < budget; ++i) {
         uint64_t idx = bricks[size_t(i)].index;
         chosen[size_t(idx)] = 1;
@@ -257,53 +153,20 @@ int compress(const float* data, const int32_t dims[3], int voxel_type, double qu
         ++voxels_activated;
     if ((cx1 | cy1 | cz1) != 0 && !chosen[brick_of(cx1, cy1, cz1)])
         ++voxels_activated;
+    budget_out = budget;
+}
 
-    // 5 + 6a. per-leaf-block decision (activate_brick, corners, leaf-level prune)
+// Stages 6b-7 of compress + the container up to the leaf section (tree.hpp:338-375,
+// frozen.hpp:144-218, io.hpp:121-165): lower-node prune, z,y,x-ordered indices, header / root /
+// upper / lower records. `out` is sized for the whole container (zero-filled); the leaf records go
+// at out + leaf_offset, record leaf_index[block] for every kLeaf / kCornerLeaf block.
+void write_tree(const int32_t dims[3], int voxel_type, float bg, float vmin, float vmax,
+                const std::vector<uint8_t>& state, const std::vector<float>& tile_val, int nt,
+                std::vector<uint8_t>& out, std::vector<uint32_t>& leaf_index, uint64_t& n_leaf_out,
+                uint64_t& leaf_offset)
+{
     const int lx = (dims[0] + 7) / 8, ly = (dims[1] + 7) / 8, lz = (dims[2] + 7) / 8;
     const int64_t nblk = int64_t(lx) * ly * lz;
-    std::vector<uint8_t> state(size_t(nblk), kAbsent);
-    std::vector<float> tile_val(size_t(nblk), 0.0f);
-    auto is_corner_block = [&](int bx, int by, int bz) {
-        return (bx == 0 && by == 0 && bz == 0) || (bx == cx1 / 8 && by == cy1 / 8 && bz == cz1 / 8);
-    };
-    parallel_for(nblk, nt, [&](int64_t b, int64_t e, int) {
-        for (int64_t i = b; i < e; ++i) {
-            int bx = int(i % lx), by = int((i / lx) % ly), bz = int(i / (int64_t(lx) * ly));
-            int x0 = bx * 8, y0 = by * 8, z0 = bz * 8;
-            bool corner = is_corner_block(bx, by, bz);
-            uint8_t st = kAbsent;
-            if (chosen[brick_of(x0, y0, z0)]) {
-                bool full = x0 + 8 <= dims[0] && y0 + 8 <= dims[1] && z0 + 8 <= dims[2];
-                if (!full) {
-                    st = kLeaf; // set_voxel path: partially active, never collapses
-                } else {
-                    bool all_bg = true, uniform = true;
-                    float v0 = v.at(x0, y0, z0);
-                    for (int z = 0; z < 8; ++z)
-                        for (int y = 0; y < 8; ++y) {
-                            const float* row = v.row(x0, y0 + y, z0 + z);
-                            for (int x = 0; x < 8; ++x) {
-                                float s = nz(row[x]);
-                                all_bg &= !(s != bg);
-                                uniform &= !(s != v0);
-                            }
-                        }
-                    if (!all_bg) {
-                        if (uniform) {
-                            st = kTile; // fully active uniform leaf -> lower tile (v0 != B)
-                            tile_val[size_t(i)] = v0;
-                        } else {
-                            st = kLeaf;
-                        }
-                    }
-                }
-            }
-            if (corner && st == kAbsent)
-                st = kCornerLeaf; // corner set_voxel creates a background leaf, partially active
-            state[size_t(i)] = st;
-        }
-    });
-
     // 6b. lower-level prune: lower regions (128^3) collapse / vanish (tree.hpp:338-375)
     const int wx = (dims[0] + 127) / 128, wy = (dims[1] + 127) / 128, wz = (dims[2] + 127) / 128;
     const int64_t nlow = int64_t(wx) * wy * wz;
@@ -351,7 +214,7 @@ int compress(const float* data, const int32_t dims[3], int voxel_type, double qu
     });
 
     // 7. indices in (z,y,x) origin order (frozen.hpp:144-173)
-    std::vector<uint32_t> leaf_index(size_t(nblk), 0);
+    leaf_index.assign(size_t(nblk), 0);
     uint64_t n_leaf = 0;
     for (int64_t i = 0; i < nblk; ++i)
         if (state[size_t(i)] == kLeaf || state[size_t(i)] == kCornerLeaf) {
@@ -457,6 +320,187 @@ int compress(const float* data, const int32_t dims[3], int voxel_type, double qu
                     }
         }
     });
+    n_leaf_out = n_leaf;
+    leaf_offset = uint64_t(leaf - o);
+}
+
+int compress(const float* data, const int32_t dims[3], int voxel_type, double quality, int metric,
+             int threads, std::vector<uint8_t>& out, svdbgpu_compress_report* rep)
+{
+    if (!(quality >= 0.0 && quality <= 1.0))
+        return fail(Errc::invalid_quality, "quality must be in [0,1]");
+    if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1)
+        return fail(Errc::size_mismatch, "volume dims must be positive");
+    if (voxel_type != 0 && voxel_type != 1)
+        return fail(Errc::size_mismatch, "voxel_type must be 0 (u8) or 1 (f32)");
+    const Vol v{data, dims[0], dims[1], dims[2]};
+    const int64_t nvox = int64_t(dims[0]) * dims[1] * dims[2];
+    const int nt = resolve_threads(threads);
+    const int64_t rows = int64_t(dims[1]) * dims[2];
+
+    // 1. min / max / finiteness (volume.hpp:41-62)
+    std::vector<float> tmin(size_t(nt), std::numeric_limits<float>::infinity());
+    std::vector<float> tmax(size_t(nt), -std::numeric_limits<float>::infinity());
+    std::atomic<bool> nonfinite{false};
+    parallel_for(rows, nt, [&](int64_t b, int64_t e, int t) {
+        float mn = tmin[size_t(t)], mx = tmax[size_t(t)];
+        for (int64_t r = b; r < e; ++r) {
+            const float* row = data + size_t(r) * size_t(dims[0]);
+            for (int x = 0; x < dims[0]; ++x) {
+                float s = nz(row[x]);
+                if (!std::isfinite(s))
+                    nonfinite = true;
+                mn = std::min(mn, s);
+                mx = std::max(mx, s);
+            }
+        }
+        tmin[size_t(t)] = mn;
+        tmax[size_t(t)] = mx;
+    });
+    if (nonfinite)
+        return fail(Errc::non_finite_voxel, "volume contains NaN or Inf");
+    float vmin = std::numeric_limits<float>::infinity(), vmax = -vmin;
+    for (int t = 0; t < nt; ++t) {
+        vmin = std::min(vmin, tmin[size_t(t)]);
+        vmax = std::max(vmax, tmax[size_t(t)]);
+    }
+
+    // 2. histogram + background (volume.hpp:177-222)
+    const int bins = voxel_type == 0 ? 256 : 1024;
+    const double hlo = vmin, hhi = vmax;
+    auto bin_of = [&](double s) {
+        if (hhi <= hlo)
+            return 0;
+        int b = int(std::floor((s - hlo) / (hhi - hlo) * double(bins)));
+        return std::clamp(b, 0, bins - 1);
+    };
+    std::vector<std::vector<uint64_t>> th(size_t(nt), std::vector<uint64_t>(size_t(bins), 0));
+    parallel_for(rows, nt, [&](int64_t b, int64_t e, int t) {
+        auto& h = th[size_t(t)];
+        for (int64_t r = b; r < e; ++r) {
+            const float* row = data + size_t(r) * size_t(dims[0]);
+            for (int x = 0; x < dims[0]; ++x)
+                ++h[size_t(bin_of(nz(row[x])))];
+        }
+    });
+    std::vector<uint64_t> hist(size_t(bins), 0);
+    for (auto& h : th)
+        for (int i = 0; i < bins; ++i)
+            hist[size_t(i)] += h[size_t(i)];
+    int best_bin = 0;
+    for (int i = 1; i < bins; ++i)
+        if (hist[size_t(i)] > hist[size_t(best_bin)])
+            best_bin = i;
+    std::vector<std::unordered_map<float, uint64_t>> exact(static_cast<size_t>(nt));
+    parallel_for(rows, nt, [&](int64_t b, int64_t e, int t) {
+        auto& m = exact[size_t(t)];
+        for (int64_t r = b; r < e; ++r) {
+            const float* row = data + size_t(r) * size_t(dims[0]);
+            for (int x = 0; x < dims[0]; ++x) {
+                float s = nz(row[x]);
+                if (bin_of(s) == best_bin)
+                    ++m[s];
+            }
+        }
+    });
+    for (int t = 1; t < nt; ++t)
+        for (auto& [val, cnt] : exact[size_t(t)])
+            exact[0][val] += cnt;
+    bool have = false;
+    float bg = 0.0f;
+    uint64_t best_count = 0;
+    for (auto& [val, cnt] : exact[0])
+        if (!have || cnt > best_count || (cnt == best_count && val < bg)) {
+            have = true;
+            bg = val;
+            best_count = cnt;
+        }
+
+    // 3. brick ranges (compress.hpp:97-145)
+    const int nbx = (dims[0] + kBrick - 1) / kBrick, nby = (dims[1] + kBrick - 1) / kBrick,
+              nbz = (dims[2] + kBrick - 1) / kBrick;
+    const int64_t total = int64_t(nbx) * nby * nbz;
+    std::vector<float> blo(static_cast<size_t>(total)), bhi(static_cast<size_t>(total));
+    parallel_for(total, nt, [&](int64_t b, int64_t e, int) {
+        for (int64_t i = b; i < e; ++i) {
+            int bx = int(i % nbx), by = int((i / nbx) % nby), bz = int(i / (int64_t(nbx) * nby));
+            int x0 = bx * kBrick, y0 = by * kBrick, z0 = bz * kBrick;
+            int x1 = std::min(x0 + kBrick, dims[0]), y1 = std::min(y0 + kBrick, dims[1]),
+                z1 = std::min(z0 + kBrick, dims[2]);
+            float mn = std::numeric_limits<float>::infinity(), mx = -mn;
+            for (int z = z0; z < z1; ++z)
+                for (int y = y0; y < y1; ++y) {
+                    const float* row = v.row(x0, y, z);
+                    for (int x = 0; x < x1 - x0; ++x) {
+                        float s = nz(row[x]);
+                        mn = std::min(mn, s);
+                        mx = std::max(mx, s);
+                    }
+                }
+            blo[size_t(i)] = mn;
+            bhi[size_t(i)] = mx;
+        }
+    });
+    // 4. total order + budget
+    std::vector<uint8_t> chosen;
+    uint64_t budget = 0, voxels_activated = 0;
+    choose_bricks(dims, blo.data(), bhi.data(), bg, metric, quality, chosen, budget, voxels_activated);
+    auto brick_of = [&](int x, int y, int z) {
+        return size_t(x / kBrick) + size_t(nbx) * (size_t(y / kBrick) + size_t(nby) * size_t(z / kBrick));
+    };
+    const int cx1 = dims[0] - 1, cy1 = dims[1] - 1, cz1 = dims[2] - 1;
+
+    // 5 + 6a. per-leaf-block decision (activate_brick, corners, leaf-level prune)
+    const int lx = (dims[0] + 7) / 8, ly = (dims[1] + 7) / 8, lz = (dims[2] + 7) / 8;
+    const int64_t nblk = int64_t(lx) * ly * lz;
+    std::vector<uint8_t> state(size_t(nblk), kAbsent);
+    std::vector<float> tile_val(size_t(nblk), 0.0f);
+    auto is_corner_block = [&](int bx, int by, int bz) {
+        return (bx == 0 && by == 0 && bz == 0) || (bx == cx1 / 8 && by == cy1 / 8 && bz == cz1 / 8);
+    };
+    parallel_for(nblk, nt, [&](int64_t b, int64_t e, int) {
+        for (int64_t i = b; i < e; ++i) {
+            int bx = int(i % lx), by = int((i / lx) % ly), bz = int(i / (int64_t(lx) * ly));
+            int x0 = bx * 8, y0 = by * 8, z0 = bz * 8;
+            bool corner = is_corner_block(bx, by, bz);
+            uint8_t st = kAbsent;
+            if (chosen[brick_of(x0, y0, z0)]) {
+                bool full = x0 + 8 <= dims[0] && y0 + 8 <= dims[1] && z0 + 8 <= dims[2];
+                if (!full) {
+                    st = kLeaf; // set_voxel path: partially active, never collapses
+                } else {
+                    bool all_bg = true, uniform = true;
+                    float v0 = v.at(x0, y0, z0);
+                    for (int z = 0; z < 8; ++z)
+                        for (int y = 0; y < 8; ++y) {
+                            const float* row = v.row(x0, y0 + y, z0 + z);
+                            for (int x = 0; x < 8; ++x) {
+                                float s = nz(row[x]);
+                                all_bg &= !(s != bg);
+                                uniform &= !(s != v0);
+                            }
+                        }
+                    if (!all_bg) {
+                        if (uniform) {
+                            st = kTile; // fully active uniform leaf -> lower tile (v0 != B)
+                            tile_val[size_t(i)] = v0;
+                        } else {
+                            st = kLeaf;
+                        }
+                    }
+                }
+            }
+            if (corner && st == kAbsent)
+                st = kCornerLeaf; // corner set_voxel creates a background leaf, partially active
+            state[size_t(i)] = st;
+        }
+    });
+
+    std::vector<uint32_t> leaf_index;
+    uint64_t n_leaf = 0, leaf_offset = 0;
+    write_tree(dims, voxel_type, bg, vmin, vmax, state, tile_val, nt, out, leaf_index, n_leaf, leaf_offset);
+    const uint64_t total_bytes = out.size();
+    uint8_t* leaf = out.data() + leaf_offset;
     parallel_for(nblk, nt, [&](int64_t b, int64_t e, int) {
         for (int64_t i = b; i < e; ++i) {
             if (state[size_t(i)] != kLeaf && state[size_t(i)] != kCornerLeaf)
@@ -564,6 +608,15 @@ struct Octave {
     }
 };
 
+inline float quantise_u8(double v)
+{
+    double c = std::clamp(v, 0.0, 1.0);
+    int b = int(std::lround(c * 255.0));
+    return float(b) / 255.0f; // load_raw's u8 mapping (volume.hpp:97)
+}
+
+} // namespace
+
 // Sparse-field (C4) threshold on d = 0.5 + 0.5 fBm per volume size (max dimension): 35% of the 8^3
 // leaf blocks hold a voxel above it. Calibrated at seed 4 from the exact per-block
 // maxima of d (tools/calibrate_sparse.py: 65th percentile); log2-linear between calibrated sizes.
@@ -584,15 +637,6 @@ double sparse_threshold(int dim_max)
     }
     return th[n - 1];
 }
-
-inline float quantise_u8(double v)
-{
-    double c = std::clamp(v, 0.0, 1.0);
-    int b = int(std::lround(c * 255.0));
-    return float(b) / 255.0f; // load_raw's u8 mapping (volume.hpp:97)
-}
-
-} // namespace
 
 int synth(int kind, const int32_t dims[3], uint64_t seed, int threads, float* out)
 {

@@ -25,6 +25,13 @@
 #include <cstdio>
 #include <cstring>
 
+#ifndef SVDB_TD_INV
+#define SVDB_TD_INV 1
+#endif
+#ifndef SVDB_CAMTAB
+#define SVDB_CAMTAB 1
+#endif
+
 namespace svdbgpu {
 
 namespace {
@@ -502,6 +509,9 @@ struct SharedDda {
                 continue;
             }
             const double inv = 1.0 / d;
+#if SVDB_TD_INV
+            cd(3 + a) = inv; // kept for t_delta below
+#endif
             double ta = (0.0 - o) * inv, tb = (h - o) * inv;
             if (ta > tb) {
                 const double tt = ta;
@@ -527,7 +537,12 @@ struct SharedDda {
             if (d != 0.0) {
                 step = d > 0.0 ? 1 : -1;
                 tn = (double(d > 0.0 ? c + 1 : c) * cell - o) / d;
+#if SVDB_TD_INV
+                // cell is a power of two, so +-cell * RN(1/d) == RN(+-cell / d) exactly (dda.hpp:80, 84)
+                td = (d > 0.0 ? cell : -cell) * cd(3 + a);
+#else
                 td = (d > 0.0 ? cell : -cell) / d;
+#endif
             }
             ci(a) = c;
             ci(3 + a) = step;
@@ -593,6 +608,16 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
 
     Tracer<CODEC> tr(A, s_ent);
     Rng rng{0};
+#if SVDB_GLIBC_LOG == 2
+    // the step log's 2 KB reduction table (log_glibc.h) staged in shared memory
+    __shared__ LogTabEntry s_logtab_buf[128];
+    for (int i = threadIdx.x; i < 128; i += blockDim.x)
+        s_logtab_buf[i] = kLogTabDev[i];
+    __syncthreads();
+    const LogTabEntry* s_logtab = s_logtab_buf;
+#else
+    const LogTabEntry* s_logtab = nullptr;
+#endif
     // The flight's ray is read only by the gather and written only at path start / scatter: kept
     // in shared memory (SoA) so the advance loop does not hold its 12 registers.
     __shared__ double s_ray[6][T];
@@ -627,14 +652,18 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     unsigned st_empty = 0, st_full = 0;
 #endif
     // Per-lane state touched only at sample start/end, scatter and pixel output lives in shared
-    // memory (SoA, conflict-free). rows 0..6: acc0..2, tp0..2, t_ev; ratio tracking adds L0..2, Tr
-    // (pathtrace aliases those names to row 6, written only by the initialisation below, before t_ev)
-    __shared__ double s_cold_d[RATIO ? 11 : 7][T];
+    // memory (SoA, conflict-free). rows: acc0..2 (whole-pixel items only; chunked items write each
+    // sample to sbuf), tp0..2, t_ev; ratio tracking adds L0..2, Tr. Names without a row of their own
+    // alias the t_ev row and are written only by the initialisation below, before t_ev.
+    constexpr int kA = CHUNK ? 0 : 3;
+    __shared__ double s_cold_d[kA + 4 + (RATIO ? 4 : 0)][T];
     __shared__ int s_cold_i[6 + (RATIO ? 1 : 0) + (CHUNK ? 1 : 0)][T];
-    volatile double &acc0 = s_cold_d[0][tid], &acc1 = s_cold_d[1][tid], &acc2 = s_cold_d[2][tid];
-    volatile double &tp0 = s_cold_d[3][tid], &tp1 = s_cold_d[4][tid], &tp2 = s_cold_d[5][tid];
-    volatile double& t_ev = s_cold_d[6][tid];
-    constexpr int kR0 = RATIO ? 7 : 6, kR = RATIO ? 1 : 0;
+    constexpr int kAcc = CHUNK ? kA + 3 : 0;
+    volatile double &acc0 = s_cold_d[kAcc][tid], &acc1 = s_cold_d[kAcc + (CHUNK ? 0 : 1)][tid],
+                    &acc2 = s_cold_d[kAcc + (CHUNK ? 0 : 2)][tid];
+    volatile double &tp0 = s_cold_d[kA][tid], &tp1 = s_cold_d[kA + 1][tid], &tp2 = s_cold_d[kA + 2][tid];
+    volatile double& t_ev = s_cold_d[kA + 3][tid];
+    constexpr int kR0 = RATIO ? kA + 4 : kA + 3, kR = RATIO ? 1 : 0;
     volatile double &L0 = s_cold_d[kR0][tid], &L1 = s_cold_d[kR0 + kR][tid], &L2 = s_cold_d[kR0 + 2 * kR][tid];
     volatile double& Tr = s_cold_d[kR0 + 3 * kR][tid];
     volatile int& have_d = s_cold_i[RATIO ? 6 : 0][tid];              // ratio: event pending (0/1)
@@ -711,7 +740,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             }
 #pragma unroll 1
             for (int k = 0; k < 3; ++k) // one division site (render.hpp:184)
-                s_cold_d[3 + k][tid] /= survive;
+                s_cold_d[kA + k][tid] /= survive;
         }
         state = kNeedSegment;
     };
@@ -748,21 +777,40 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             if (s == A.spp) {
 #pragma unroll 1
                 for (int k = 0; k < 3; ++k) // render.hpp:308-310, one division site
-                    A.out[out_off + k] = float(s_cold_d[k][tid] / double(A.spp));
+                    A.out[out_off + k] = float(s_cold_d[CHUNK ? kAcc : k][tid] / double(A.spp));
                 state = kNeedPixel;
                 return;
             }
-            rng = Rng::for_pixel_sample(A.seed_mixed, px, py, s);
-            double jx = 0.0, jy = 0.0;
-#pragma unroll 1
-            for (int k = 0; k < 2; ++k) { // jitter draws (render.hpp:300-301), one generator copy
-                const double u = rng.uniform();
-                if (k == 0)
-                    jx = u;
-                else
-                    jy = u;
+            bool from_table = false;
+            if constexpr (CHUNK && SVDB_CAMTAB) {
+                if (A.camtab) { // ray and post-jitter stream from k_camera_rays (same arithmetic)
+                    const double2* rec = A.camtab + 2 * (size_t(out_off / 3) * size_t(A.spp) + size_t(s));
+                    const double2 a = __ldg(rec), b = __ldg(rec + 1);
+                    rng.state = uint64_t(__double_as_longlong(b.y));
+                    Ray r;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k)
+                        r.o[k] = A.cam.pos[k];
+                    r.d[0] = a.x;
+                    r.d[1] = a.y;
+                    r.d[2] = b.x;
+                    ray_store(r);
+                    from_table = true;
+                }
             }
-            ray_store(camera_ray(A.cam, double(px) + jx, double(py) + jy));
+            if (!from_table) {
+                rng = Rng::for_pixel_sample(A.seed_mixed, px, py, s);
+                double jx = 0.0, jy = 0.0;
+#pragma unroll 1
+                for (int k = 0; k < 2; ++k) { // jitter draws (render.hpp:300-301), one generator copy
+                    const double u = rng.uniform();
+                    if (k == 0)
+                        jx = u;
+                    else
+                        jy = u;
+                }
+                ray_store(camera_ray(A.cam, double(px) + jx, double(py) + jy));
+            }
             tp0 = tp1 = tp2 = 1.0;
             bounces = 0;
             if constexpr (RATIO)
@@ -795,7 +843,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         // the step draw's log does not depend on the DDA: compute it from the next uniform before
         // the cell lookup (independent FP64 chains interleave); the draw is consumed only if the
         // cell has draws, so the stream is unchanged
-        const double lg = step_log(1.0 - rng.peek());
+        const double lg = step_log(1.0 - rng.peek(), s_logtab);
         if constexpr (HDDA) {
             if (state == kNeedRegion) { // next lower-node region; one without draws is skipped whole
                 int rc[3];
@@ -917,7 +965,8 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                     } else {
                         s = 0;
                     }
-                    acc0 = acc1 = acc2 = 0.0;
+                    if constexpr (!CHUNK)
+                        acc0 = acc1 = acc2 = 0.0;
                     state = kNeedPath;
                 }
             }
@@ -965,6 +1014,34 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     atomicAdd(A.counters + 12, (unsigned long long)st_empty); // macrocell visits: empty / non-empty
     atomicAdd(A.counters + 13, (unsigned long long)st_full);
 #endif
+}
+
+// Camera rays of a sample-chunked render, precomputed at full SIMD width (in k_trace a new path's
+// camera ray ran with ~3 of 32 lanes active): per (pixel, sample) of this rank's tiles, the
+// reference's per-sample prologue (render.hpp:298-302: Rng::for_pixel_sample, jitter jx, jy,
+// camera_ray) with the same arithmetic as k_trace's in-kernel path. Record = ray direction and the
+// RNG state after the two jitter draws; the origin is the camera position.
+__global__ void k_camera_rays(const __grid_constant__ RenderArgs A, long long ntiles, double2* __restrict__ tab)
+{
+    const long long n = ntiles * 256 * A.spp;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long slot = i / A.spp;
+        const int s = int(i - slot * A.spp);
+        const long long k = slot >> 8;
+        const int lx = int(slot & 15), ly = int((slot >> 4) & 15);
+        const long long t = k * A.nranks + A.rank;
+        const int px = int(t % A.tiles_x) * 16 + lx, py = int(t / A.tiles_x) * 16 + ly;
+        if (px >= A.cam.w || py >= A.cam.h)
+            continue;
+        const size_t pix = A.packed ? size_t(slot) : size_t(py) * size_t(A.cam.w) + size_t(px);
+        Rng rng = Rng::for_pixel_sample(A.seed_mixed, px, py, s);
+        const double jx = rng.uniform();
+        const double jy = rng.uniform();
+        const Ray r = camera_ray(A.cam, double(px) + jx, double(py) + jy);
+        double2* o = tab + 2 * (pix * size_t(A.spp) + size_t(s));
+        o[0] = make_double2(r.d[0], r.d[1]);
+        o[1] = make_double2(r.d[2], __longlong_as_double((long long)rng.state));
+    }
 }
 
 __global__ void k_unpack(const float* __restrict__ packed, int nranks, long long max_tiles, int w, int h, int tiles_x,
@@ -1168,6 +1245,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     // of a pixel, not all spp, so the last items of a frame are short (the frame's tail shrinks
     // from ~spp to ~chunk path lengths); per-sample results go through sbuf to k_reduce
     A.sbuf = nullptr;
+    A.camtab = nullptr;
     A.chunk = 0;
     A.nchunks = 1;
     if (wave && ntiles > 0) {
@@ -1189,6 +1267,17 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
             A.sbuf = g->d_sbuf;
             A.chunk = chunk;
             A.nchunks = (st->spp + chunk - 1) / chunk;
+            const size_t tab = npix * size_t(st->spp) * 32;
+            if (SVDB_CAMTAB && tab <= (size_t(16) << 30)) {
+                if (tab > g->camtab_cap || !g->d_camtab) {
+                    cudaFree(g->d_camtab);
+                    g->d_camtab = nullptr;
+                    g->camtab_cap = 0;
+                    SVDB_CUDA(cudaMalloc(&g->d_camtab, tab));
+                    g->camtab_cap = tab;
+                }
+                A.camtab = g->d_camtab;
+            }
         }
     }
     if (ntiles > 0) {
@@ -1217,6 +1306,11 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         if (wave) LAUNCH_T(C, SVDBGPU_MODE_RATIO) else LAUNCH_R(C, SVDBGPU_MODE_RATIO);         \
         break;                                                                                 \
     }
+        if (A.camtab && !fp32) {
+            const long long n = ntiles * 256 * st->spp;
+            k_camera_rays<<<unsigned(std::min<long long>((n + 255) / 256, 148LL * 32)), 256, 0, s>>>(
+                A, ntiles, g->d_camtab);
+        }
         if (fp32)
             launch_trace_fast(A, g->codec, st->mode, st->precision, n_units, smem, s);
         else switch (g->codec) {
@@ -1274,7 +1368,8 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         stats->lookups = samples * 8;
         stats->render_ms = rms;
         stats->macrocell_ms = double(range_ms) + double(mms);
-        stats->launches = (range_ms > 0.0f ? 1u : 0u) + 1u + (hdda ? 1u : 0u) + (ntiles > 0 ? 1u : 0u) + (A.chunk ? 1u : 0u);
+        stats->launches = (range_ms > 0.0f ? 1u : 0u) + 1u + (hdda ? 1u : 0u) + (ntiles > 0 ? 1u : 0u) + (A.chunk ? 1u : 0u) +
+                          (A.camtab && !fp32 ? 1u : 0u);
     }
     return 0;
 }

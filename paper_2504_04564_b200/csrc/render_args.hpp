@@ -48,6 +48,9 @@ struct RenderArgs {
     // whole pixel and accumulates in place.
     float* sbuf;
     int chunk, nchunks;
+    // sample-chunked renders: camera rays precomputed at full SIMD width by k_camera_rays, per
+    // (pixel, sample) as sbuf: {d.x, d.y}, {d.z, RNG state after the two jitter draws} (32 B)
+    const double2* camtab;
 };
 
 // FP32-arithmetic tracking kernel launch (render_fast.cu): SVDBGPU_PRECISION_FP32 (all FP32) or

@@ -35,5 +35,16 @@ void parallel_for(int64_t n, int threads, const std::function<void(int64_t, int6
 int compress(const float* data, const int32_t dims[3], int voxel_type, double quality, int metric,
              int threads, std::vector<uint8_t>& out, svdbgpu_compress_report* rep);
 int synth(int kind, const int32_t dims[3], uint64_t seed, int threads, float* out);
+double sparse_threshold(int dim_max);
+
+// Encoder stages shared by the dense compress() and the streaming device encoder (stream_encoder.cu).
+constexpr int kEncBrick = 32; // compress.hpp brick edge
+enum : uint8_t { kBlkAbsent = 0, kBlkLeaf = 1, kBlkTile = 2, kBlkCornerLeaf = 3 }; // per 8^3 leaf block
+void choose_bricks(const int32_t dims[3], const float* blo, const float* bhi, float bg, int metric, double quality,
+                   std::vector<uint8_t>& chosen, uint64_t& budget, uint64_t& voxels_activated);
+void write_tree(const int32_t dims[3], int voxel_type, float bg, float vmin, float vmax,
+                const std::vector<uint8_t>& state, const std::vector<float>& tile_val, int threads,
+                std::vector<uint8_t>& out, std::vector<uint32_t>& leaf_index, uint64_t& n_leaf,
+                uint64_t& leaf_offset);
 
 } // namespace svdbgpu
