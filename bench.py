@@ -127,9 +127,23 @@ def scene_for(args):
     return replace(sc, width=args.width or sc.width, height=args.height or sc.height, settings=st)
 
 
-def build_grid_bytes(sc, threads):
-    """Product host encoder: svdbgpu_synth + svdbgpu_compress (byte-identical to the reference)."""
+def peak_rss_gb():
+    import resource
+    return resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6  # ru_maxrss is in KB on Linux
+
+
+def build_grid_bytes(sc, threads, device=0):
+    """The grid's SVDB v1 bytes (byte-identical to the reference's compress + serialize_frozen). The
+    fBm-based volumes go through the streaming device encoder (svdbgpu_synth_compress: no dense host
+    array); Marschner-Lobb (host libm) through svdbgpu_synth + the native host encoder."""
     import paper_2504_04564_b200 as P
+    if sc.volume != "marschner_lobb" and P.device_count() > device:
+        svdb, rep, sec = P.synth_compress(sc.volume, sc.dims, sc.volume_seed, P.CompressionParams(1.0), device=device)
+        info = {"encoder": "streaming device encoder (svdbgpu_synth_compress, 32-slice slabs)", "encode_s": sec,
+                "peak_host_rss_gb": peak_rss_gb(), "n_leaf": int(np.frombuffer(svdb[52:60], np.uint64)[0])}
+        log(f"[bench] streaming encode {sc.dims} {sec:.1f}s -> {len(svdb) / 1e9:.3f} GB SVDB, "
+            f"peak host RSS {info['peak_host_rss_gb']:.1f} GB")
+        return svdb, info
     t0 = time.perf_counter()
     vol = P.synth(sc.volume, sc.dims, sc.volume_seed, threads=threads)
     t1 = time.perf_counter()
@@ -137,17 +151,18 @@ def build_grid_bytes(sc, threads):
     t2 = time.perf_counter()
     log(f"[bench] synth {sc.dims} {t1 - t0:.1f}s, compress {t2 - t1:.1f}s -> {len(svdb) / 1e9:.3f} GB SVDB")
     del vol
-    return svdb, {"synth_s": t1 - t0, "compress_s": t2 - t1}
+    return svdb, {"encoder": "host (svdbgpu_synth + svdbgpu_compress)", "synth_s": t1 - t0, "compress_s": t2 - t1,
+                  "peak_host_rss_gb": peak_rss_gb()}
 
 
-def shared_grid_bytes(sc, rank, world, dist, threads):
+def shared_grid_bytes(sc, rank, world, dist, threads, device=0):
     """Encode once: rank 0 builds the SVDB and publishes it in /dev/shm, the other ranks map it."""
     if world == 1:
-        return build_grid_bytes(sc, threads)
+        return build_grid_bytes(sc, threads, device)
     path = f"/dev/shm/svdb_bench_{os.environ.get('MASTER_PORT', '0')}_{sc.name}.svdb"
     info = {}
     if rank == 0:
-        svdb, info = build_grid_bytes(sc, threads)
+        svdb, info = build_grid_bytes(sc, threads, device)
         tmp = path + ".tmp"
         with open(tmp, "wb") as f:
             f.write(svdb)
@@ -411,7 +426,7 @@ def run_ours(args):
     sc = scene_for(args)
     cam = sc.camera()
     host_threads = max(1, os.cpu_count() or 1)
-    svdb, enc = shared_grid_bytes(sc, rank, world, dist, host_threads)
+    svdb, enc = shared_grid_bytes(sc, rank, world, dist, host_threads, local)
     t0 = time.perf_counter()
     grid = P.DeviceGrid(svdb, sc.codec, device=local)
     upload_s = time.perf_counter() - t0

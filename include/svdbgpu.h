@@ -203,6 +203,23 @@ int svdbgpu_compress(const float* data, const int32_t dims[3], int32_t voxel_typ
                      int32_t metric /*0 closest,1 farthest,2 median*/, int32_t threads,
                      uint8_t** svdb_out, size_t* n_out, svdbgpu_compress_report* report);
 
+/* ---- streaming device encoder: the same SVDB v1 bytes as svdbgpu_compress on
+ * the dense volume, without a dense host array. The volume is streamed through `device` in z-slabs of
+ * 32 slices (five passes: range + brick scan, histogram, exact background, block decisions, leaf
+ * records); host memory holds only the output container and 5 B per 8^3 block.
+ * svdbgpu_compress_stream: fn(user, z0, nz, out) fills slices [z0, z0+nz) (x fastest, dims[0]*dims[1]*nz
+ * floats) and returns 0; it is called five times per slab, in slab order, and must return the same
+ * values each time. svdbgpu_synth_compress: the svdbgpu_synth volumes of kind 1-3 generated on the
+ * device (bit-identical to svdbgpu_synth). *seconds (optional) = encode wall time. *svdb_out is freed
+ * with svdbgpu_free. */
+typedef int (*svdbgpu_slab_fn)(void* user, int32_t z0, int32_t nz, float* out);
+int svdbgpu_compress_stream(svdbgpu_slab_fn fn, void* user, const int32_t dims[3], int32_t voxel_type,
+                            double quality, int32_t metric, int32_t device, uint8_t** svdb_out, size_t* n_out,
+                            svdbgpu_compress_report* report, double* seconds);
+int svdbgpu_synth_compress(int32_t kind, const int32_t dims[3], uint64_t seed, double quality, int32_t metric,
+                           int32_t device, uint8_t** svdb_out, size_t* n_out, svdbgpu_compress_report* report,
+                           double* seconds);
+
 /* ---- quantised container: SVDB v1 -> "SVDB v2" with N-bit leaves ----
  * Same header / root / upper / lower sections as v1 (io.hpp:22-43) with version 2 and the codec in
  * the header's padding word (offset 68); each leaf record is {origin 3 x i32, pad, active mask 512

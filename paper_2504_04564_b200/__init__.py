@@ -6,5 +6,6 @@ this package is its host-side Python mirror of the reference svdb API.
 from .api import (  # noqa: F401
     Camera, Codec, CompressionParams, CompressionReport, DeviceGrid, Errc, Error, Image, Metric,
     RenderMode, RenderSettings, TransferFunction, VoxelType, compress, device_count, frame_camera,
-    nccl_version, quantise, render, render_device, render_multi, sample_device, synth, tiles_for_rank, unpack_tiles_device,
+    compress_stream, nccl_version, quantise, render, render_device, render_multi, sample_device, synth,
+    synth_compress, tiles_for_rank, unpack_tiles_device,
 )

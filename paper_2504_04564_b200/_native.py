@@ -50,6 +50,7 @@ class CompressReport(C.Structure):
 
 # exported symbol -> (restype, argtypes); tests check this list against include/svdbgpu.h
 P = C.c_void_p
+SLAB_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_float))
 SIGNATURES = {
     "svdbgpu_abi_version": (C.c_int, []),
     "svdbgpu_last_error": (C.c_char_p, []),
@@ -78,6 +79,12 @@ SIGNATURES = {
                                    C.c_int32, C.POINTER(P), C.POINTER(C.c_size_t),
                                    C.POINTER(CompressReport)]),
     "svdbgpu_synth": (C.c_int, [C.c_int32, C.POINTER(C.c_int32), C.c_uint64, C.c_int32, P]),
+    "svdbgpu_compress_stream": (C.c_int, [SLAB_FN, P, C.POINTER(C.c_int32), C.c_int32, C.c_double, C.c_int32,
+                                          C.c_int32, C.POINTER(P), C.POINTER(C.c_size_t),
+                                          C.POINTER(CompressReport), C.POINTER(C.c_double)]),
+    "svdbgpu_synth_compress": (C.c_int, [C.c_int32, C.POINTER(C.c_int32), C.c_uint64, C.c_double, C.c_int32,
+                                         C.c_int32, C.POINTER(P), C.POINTER(C.c_size_t), C.POINTER(CompressReport),
+                                         C.POINTER(C.c_double)]),
     "svdbgpu_quantise": (C.c_int, [P, C.c_size_t, C.c_int32, C.c_int32, C.POINTER(P), C.POINTER(C.c_size_t)]),
 }
 

@@ -134,6 +134,78 @@ def compress(volume: np.ndarray, params: CompressionParams = CompressionParams()
                                    rep.achieved_ratio)
 
 
+class OwnedBuffer(np.ndarray):
+    """A uint8 array over a buffer the library malloc'd (freed with svdbgpu_free when the array and
+    every view of it are gone): large containers reach Python without a copy."""
+
+    @staticmethod
+    def take(ptr, n: int) -> "OwnedBuffer":
+        import weakref
+        if n == 0:
+            N.lib().svdbgpu_free(ptr)
+            return np.zeros(0, np.uint8).view(OwnedBuffer)
+        raw = (C.c_uint8 * n).from_address(ptr.value)
+        arr = np.ctypeslib.as_array(raw).view(OwnedBuffer)
+        weakref.finalize(raw, N.lib().svdbgpu_free, C.c_void_p(ptr.value))
+        arr._raw = raw  # keeps the ctypes object (and so the finalizer) alive with the array
+        return arr
+
+
+def _report(rep) -> "CompressionReport":
+    return CompressionReport(rep.background, rep.num_bricks, rep.bricks_activated, rep.voxels_activated,
+                             rep.frozen_bytes, rep.dense_bytes, rep.achieved_ratio)
+
+
+def synth_compress(kind: str, dims: Sequence[int], seed: int = 0, params: CompressionParams = CompressionParams(),
+                   device: int = 0):
+    """The synth(kind, dims, seed) volume compressed on the GPU without a dense host array (streaming
+    device encoder, svdbgpu_synth_compress): the same bytes as compress(synth(...)). Returns
+    (SVDB v1 buffer, CompressionReport, encode seconds); kinds fbm_smoke / turbulence / sparse."""
+    dx, dy, dz = (int(d) for d in dims)
+    out = C.c_void_p()
+    n = C.c_size_t()
+    rep = N.CompressReport()
+    sec = C.c_double()
+    _check(N.lib().svdbgpu_synth_compress(SYNTH_KINDS[kind], (C.c_int32 * 3)(dx, dy, dz), seed, float(params.quality),
+                                          int(params.metric), device, C.byref(out), C.byref(n), C.byref(rep),
+                                          C.byref(sec)))
+    return OwnedBuffer.take(out, n.value), _report(rep), sec.value
+
+
+def compress_stream(slab_fn, dims: Sequence[int], params: CompressionParams = CompressionParams(),
+                    voxel_type: VoxelType = VoxelType.f32, device: int = 0):
+    """The fixed-rate encoder over a volume streamed through the GPU in 32-slice z-slabs
+    (svdbgpu_compress_stream): ``slab_fn(z0, nz)`` returns slices [z0, z0 + nz) as float32 [nz, y, x]
+    (called five times per slab, same values each time). Same bytes as compress() on the dense
+    volume. Returns (SVDB v1 buffer, CompressionReport, encode seconds)."""
+    dx, dy, dz = (int(d) for d in dims)
+    err = []
+
+    def cb(user, z0, nz, dst):
+        try:
+            a = np.ascontiguousarray(slab_fn(int(z0), int(nz)), dtype=np.float32)
+            if a.size != dx * dy * nz:
+                raise ValueError(f"slab_fn({z0}, {nz}) returned {a.size} values, want {dx * dy * nz}")
+            C.memmove(dst, a.ctypes.data, a.nbytes)
+            return 0
+        except Exception as exc:  # reported through the library as IoError
+            err.append(exc)
+            return 1
+
+    fn = N.SLAB_FN(cb)
+    out = C.c_void_p()
+    n = C.c_size_t()
+    rep = N.CompressReport()
+    sec = C.c_double()
+    rc = N.lib().svdbgpu_compress_stream(fn, None, (C.c_int32 * 3)(dx, dy, dz), int(voxel_type), float(params.quality),
+                                         int(params.metric), device, C.byref(out), C.byref(n), C.byref(rep),
+                                         C.byref(sec))
+    if rc and err:
+        raise err[0]
+    _check(rc)
+    return OwnedBuffer.take(out, n.value), _report(rep), sec.value
+
+
 def quantise(svdb: bytes, codec: "Codec" = None, device: int = 0) -> bytes:
     """SVDB v1 -> quantised SVDB v2 (leaves as N-bit codes + per-leaf lo/scale, encoded on the GPU
     with the device codec; include/svdbgpu.h ``svdbgpu_quantise``). ``DeviceGrid`` loads the result

@@ -348,16 +348,45 @@ int svdbgpu_compress(const float* data, const int32_t dims[3], int32_t voxel_typ
     if (metric < 0 || metric > 2)
         return fail_code(SVDBGPU_E_INVALID_ARG, "metric must be 0..2");
     return guarded([&] {
-        std::vector<uint8_t> bytes;
+        HostBuf bytes;
         int rc = compress(data, dims, voxel_type, quality, metric, threads, bytes, report);
         if (rc)
             return rc;
-        auto* p = static_cast<uint8_t*>(std::malloc(bytes.size()));
-        if (!p)
-            return fail_code(SVDBGPU_E_OOM, "host allocation failed");
-        std::memcpy(p, bytes.data(), bytes.size());
-        *svdb_out = p;
-        *n_out = bytes.size();
+        *n_out = bytes.n;
+        *svdb_out = bytes.release();
+        return 0;
+    });
+}
+
+int svdbgpu_compress_stream(svdbgpu_slab_fn fn, void* user, const int32_t dims[3], int32_t voxel_type, double quality,
+                            int32_t metric, int32_t device, uint8_t** svdb_out, size_t* n_out,
+                            svdbgpu_compress_report* report, double* seconds)
+{
+    if (!fn || !dims || !svdb_out || !n_out)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "null argument");
+    return guarded([&] {
+        HostBuf bytes;
+        if (int rc = stream_compress_callback(fn, user, dims, voxel_type, quality, metric, device, bytes, report,
+                                              seconds))
+            return rc;
+        *n_out = bytes.n;
+        *svdb_out = bytes.release();
+        return 0;
+    });
+}
+
+int svdbgpu_synth_compress(int32_t kind, const int32_t dims[3], uint64_t seed, double quality, int32_t metric,
+                           int32_t device, uint8_t** svdb_out, size_t* n_out, svdbgpu_compress_report* report,
+                           double* seconds)
+{
+    if (!dims || !svdb_out || !n_out)
+        return fail_code(SVDBGPU_E_INVALID_ARG, "null argument");
+    return guarded([&] {
+        HostBuf bytes;
+        if (int rc = stream_compress_synth(kind, dims, seed, quality, metric, device, bytes, report, seconds))
+            return rc;
+        *n_out = bytes.n;
+        *svdb_out = bytes.release();
         return 0;
     });
 }

@@ -404,10 +404,10 @@ __device__ __forceinline__ double tf_max_alpha_in_range(const DevTF& tf, const f
 #ifndef SVDB_GLIBC_LOG
 #define SVDB_GLIBC_LOG 0 // 1: step lengths bit-exact to the reference; measured -5% (C3) / -7% (C4)
 #endif
-__device__ __forceinline__ double step_log(double w, const LogTabEntry* smem_tab = nullptr)
+__device__ __forceinline__ double step_log(double w)
 {
 #if SVDB_GLIBC_LOG
-    return glibc_log(w, smem_tab);
+    return glibc_log(w);
 #else
     return log(w);
 #endif
@@ -441,6 +441,15 @@ struct Rng {
         return double(x >> 11) * 0x1.0p-53;
     }
     __device__ __forceinline__ void skip() { state += 0x9E3779B97F4A7C15ull; }
+    // the value the most recent uniform() / skip() consumed (pure function of the state)
+    __device__ __forceinline__ double last() const
+    {
+        uint64_t x = state;
+        x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+        x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+        x ^= x >> 31;
+        return double(x >> 11) * 0x1.0p-53;
+    }
     __device__ __forceinline__ double uniform()
     {
         state += 0x9E3779B97F4A7C15ull;

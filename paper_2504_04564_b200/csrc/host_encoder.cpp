@@ -162,8 +162,7 @@ void choose_bricks(const int32_t dims[3], const float* blo, const float* bhi, fl
 // at out + leaf_offset, record leaf_index[block] for every kLeaf / kCornerLeaf block.
 void write_tree(const int32_t dims[3], int voxel_type, float bg, float vmin, float vmax,
                 const std::vector<uint8_t>& state, const std::vector<float>& tile_val, int nt,
-                std::vector<uint8_t>& out, std::vector<uint32_t>& leaf_index, uint64_t& n_leaf_out,
-                uint64_t& leaf_offset)
+                HostBuf& out, std::vector<uint32_t>& leaf_index, uint64_t& n_leaf_out, uint64_t& leaf_offset)
 {
     const int lx = (dims[0] + 7) / 8, ly = (dims[1] + 7) / 8, lz = (dims[2] + 7) / 8;
     const int64_t nblk = int64_t(lx) * ly * lz;
@@ -243,8 +242,8 @@ void write_tree(const int32_t dims[3], int voxel_type, float bg, float vmin, flo
 
     const uint64_t total_bytes =
         kHdr + kRootRec * n_upper + kUpperRec * n_upper + kLowerRec * n_lower + kLeafRec * n_leaf;
-    out.assign(size_t(total_bytes), 0);
-    uint8_t* o = out.data();
+    out.alloc(size_t(total_bytes));
+    uint8_t* o = out.p;
     // header (io.hpp:124-137)
     std::memcpy(o, "SVDB", 4);
     put_u32(o + 4, 1);
@@ -325,7 +324,7 @@ void write_tree(const int32_t dims[3], int voxel_type, float bg, float vmin, flo
 }
 
 int compress(const float* data, const int32_t dims[3], int voxel_type, double quality, int metric,
-             int threads, std::vector<uint8_t>& out, svdbgpu_compress_report* rep)
+             int threads, HostBuf& out, svdbgpu_compress_report* rep)
 {
     if (!(quality >= 0.0 && quality <= 1.0))
         return fail(Errc::invalid_quality, "quality must be in [0,1]");
@@ -499,8 +498,8 @@ int compress(const float* data, const int32_t dims[3], int voxel_type, double qu
     std::vector<uint32_t> leaf_index;
     uint64_t n_leaf = 0, leaf_offset = 0;
     write_tree(dims, voxel_type, bg, vmin, vmax, state, tile_val, nt, out, leaf_index, n_leaf, leaf_offset);
-    const uint64_t total_bytes = out.size();
-    uint8_t* leaf = out.data() + leaf_offset;
+    const uint64_t total_bytes = out.n;
+    uint8_t* leaf = out.p + leaf_offset;
     parallel_for(nblk, nt, [&](int64_t b, int64_t e, int) {
         for (int64_t i = b; i < e; ++i) {
             if (state[size_t(i)] != kLeaf && state[size_t(i)] != kCornerLeaf)
@@ -636,6 +635,18 @@ double sparse_threshold(int dim_max)
         }
     }
     return th[n - 1];
+}
+
+void synth_lattices(int kind, const int32_t dims[3], uint64_t seed, std::vector<SynthOctave>& out)
+{
+    const int dmax = std::max(dims[0], std::max(dims[1], dims[2]));
+    const int octaves = kind == 0 ? 0 : (kind == 2 ? 6 : 5);
+    const int base_cells = kind == 2 ? 4 : 6;
+    out.clear();
+    for (int o = 0; o < octaves; ++o) {
+        Octave oc(base_cells << o, dmax, seed * 1315423911ull + uint64_t(o) + 1);
+        out.push_back(SynthOctave{oc.cells, oc.n, oc.scale, std::move(oc.lat)});
+    }
 }
 
 int synth(int kind, const int32_t dims[3], uint64_t seed, int threads, float* out)

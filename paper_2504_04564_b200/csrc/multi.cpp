@@ -223,7 +223,8 @@ extern "C" int svdbgpu_render_multi(svdbgpu_grid* const* grids, int32_t ndev, co
         SVDB_CUDA(cudaSetDevice(g0->device));
         SVDB_CUDA(cudaStreamSynchronize(g0->stream));
         float gms = 0.0f;
-        cudaEventElapsedTime(&gms, e0, e1);
+        if (ndev > 1)
+            cudaEventElapsedTime(&gms, e0, e1);
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         if (gather_ms)

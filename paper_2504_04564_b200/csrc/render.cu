@@ -25,11 +25,8 @@
 #include <cstdio>
 #include <cstring>
 
-#ifndef SVDB_TD_INV
-#define SVDB_TD_INV 1
-#endif
-#ifndef SVDB_CAMTAB
-#define SVDB_CAMTAB 1
+#ifndef SVDB_LAZY_LOG
+#define SVDB_LAZY_LOG 1
 #endif
 
 namespace svdbgpu {
@@ -472,7 +469,8 @@ __global__ void __launch_bounds__(256) k_render(const __grid_constant__ RenderAr
 // blocks per warp from a global counter (lanes refill individually, so no lane idles at a pixel
 // boundary); the grid is sized to the resident CTA count.
 enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4, kPoint = 5, kScatter = 6,
-             kNeedRegion = 7 }; // kNeedRegion: hierarchical DDA, next 128^3 lower-node region
+             kNeedRegion = 7, // hierarchical DDA: next 128^3 lower-node region
+             kNeedLog = 8 };  // tentative step whose cell-exit decision needs the exact FP64 log
 
 // The macrocell DDA of device.cuh (dda.hpp:52-109), same arithmetic, with its 23 words of
 // per-lane state in shared memory (SoA, conflict-free) instead of registers: it is touched once
@@ -509,9 +507,7 @@ struct SharedDda {
                 continue;
             }
             const double inv = 1.0 / d;
-#if SVDB_TD_INV
             cd(3 + a) = inv; // kept for t_delta below
-#endif
             double ta = (0.0 - o) * inv, tb = (h - o) * inv;
             if (ta > tb) {
                 const double tt = ta;
@@ -537,12 +533,8 @@ struct SharedDda {
             if (d != 0.0) {
                 step = d > 0.0 ? 1 : -1;
                 tn = (double(d > 0.0 ? c + 1 : c) * cell - o) / d;
-#if SVDB_TD_INV
                 // cell is a power of two, so +-cell * RN(1/d) == RN(+-cell / d) exactly (dda.hpp:80, 84)
                 td = (d > 0.0 ? cell : -cell) * cd(3 + a);
-#else
-                td = (d > 0.0 ? cell : -cell) / d;
-#endif
             }
             ci(a) = c;
             ci(3 + a) = step;
@@ -608,16 +600,6 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
 
     Tracer<CODEC> tr(A, s_ent);
     Rng rng{0};
-#if SVDB_GLIBC_LOG == 2
-    // the step log's 2 KB reduction table (log_glibc.h) staged in shared memory
-    __shared__ LogTabEntry s_logtab_buf[128];
-    for (int i = threadIdx.x; i < 128; i += blockDim.x)
-        s_logtab_buf[i] = kLogTabDev[i];
-    __syncthreads();
-    const LogTabEntry* s_logtab = s_logtab_buf;
-#else
-    const LogTabEntry* s_logtab = nullptr;
-#endif
     // The flight's ray is read only by the gather and written only at path start / scatter: kept
     // in shared memory (SoA) so the advance loop does not hold its 12 registers.
     __shared__ double s_ray[6][T];
@@ -782,7 +764,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                 return;
             }
             bool from_table = false;
-            if constexpr (CHUNK && SVDB_CAMTAB) {
+            if constexpr (CHUNK) {
                 if (A.camtab) { // ray and post-jitter stream from k_camera_rays (same arithmetic)
                     const double2* rec = A.camtab + 2 * (size_t(out_off / 3) * size_t(A.spp) + size_t(s));
                     const double2 a = __ldg(rec), b = __ldg(rec + 1);
@@ -843,7 +825,14 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         // the step draw's log does not depend on the DDA: compute it from the next uniform before
         // the cell lookup (independent FP64 chains interleave); the draw is consumed only if the
         // cell has draws, so the stream is unchanged
-        const double lg = step_log(1.0 - rng.peek(), s_logtab);
+#if SVDB_LAZY_LOG
+        // a float lower bound of the step length -ln(1 - u) from the next uniform (MUFU lg2:
+        // |error| <= 4e-7 (1 + y); bound taken 10x wider), computed before the cell lookup
+        const float y = -__log2f(float(1.0 - rng.peek())) * 0.693147182f;
+        const float y_lb = y - (4e-6f + 4e-6f * y);
+#else
+        const double lg = step_log(1.0 - rng.peek());
+#endif
         if constexpr (HDDA) {
             if (state == kNeedRegion) { // next lower-node region; one without draws is skipped whole
                 int rc[3];
@@ -890,7 +879,25 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             tb = tbb;
         }
         rng.skip();
+#if SVDB_LAZY_LOG
+        // The step leaves the cell when t - ln(1-u) * inv >= tb, and then only that decision is
+        // used, never the new t (the next non-empty cell restarts at its entry, render.hpp:113-118).
+        // When the float bound already clears the gap with margin (>= 1e-6 relative, far above every
+        // rounding error) the decision is certain: no FP64 log. Otherwise the exact step is taken in
+        // the gather phase (kNeedLog), batched with the collisions it mostly leads to.
+        if (y_lb * float(inv) * 0.999999f > float(tb - t) * 1.000001f) {
+            state = kNeedCell;
+            return;
+        }
+        state = kNeedLog;
+#else
         t -= lg * inv;
+        state = t >= tb ? kNeedCell : kPoint;
+#endif
+    };
+    // kNeedLog: the exact step with the reference's FP64 log of the draw just consumed (render.hpp:116)
+    auto do_exact_step = [&]() {
+        t -= step_log(1.0 - rng.last()) * inv;
         state = t >= tb ? kNeedCell : kPoint;
     };
     // accept test on the gathered value (render.hpp:119-122) / ratio update
@@ -982,7 +989,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             continue; // finished lanes idle until the whole warp is done
         // ---- phase selection: run the one phase most lanes are waiting in; ties go to the
         // gather so its memory latency is paid by as many lanes as possible at once ----
-        const int nS = __popc(__ballot_sync(live, state == kPoint));
+        const int nS = __popc(__ballot_sync(live, state == kPoint || state == kNeedLog));
         const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell || state == kNeedRegion));
         const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter));
         const int phase = (nS > 0 && nS >= nA && nS >= nT) || (nA == 0 && nT == 0) ? 2 : (nA >= nT ? 1 : 0);
@@ -1000,8 +1007,11 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
 #pragma unroll 1
             for (int k = 0; k < kAdvIters && (state == kNeedCell || state == kInCell || state == kNeedRegion); ++k)
                 do_advance();
-        } else if (state == kPoint) {
-            do_sample();
+        } else {
+            if (state == kNeedLog)
+                do_exact_step();
+            if (state == kPoint)
+                do_sample();
         }
     }
     unsigned long long s64 = tr.samples;
@@ -1268,7 +1278,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
             A.chunk = chunk;
             A.nchunks = (st->spp + chunk - 1) / chunk;
             const size_t tab = npix * size_t(st->spp) * 32;
-            if (SVDB_CAMTAB && tab <= (size_t(16) << 30)) {
+            if (tab <= (size_t(16) << 30)) {
                 if (tab > g->camtab_cap || !g->d_camtab) {
                     cudaFree(g->d_camtab);
                     g->d_camtab = nullptr;
