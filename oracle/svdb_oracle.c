@@ -524,8 +524,12 @@ typedef struct {
     int in_fine;
 } flight_t;
 
+static __thread int g_trace;
+#include <stdio.h>
 static int flight_init(const mc_t* mc, const ray_t* r, flight_t* f)
 {
+    if (g_trace)
+        fprintf(stderr, "[oracle] ray %a %a %a %a %a %a\n", r->o[0], r->o[1], r->o[2], r->d[0], r->d[1], r->d[2]);
     f->mc = mc;
     f->ray = r;
     f->in_fine = 0;
@@ -536,7 +540,21 @@ static int flight_init(const mc_t* mc, const ray_t* r, flight_t* f)
     return dda_init_cells(mc->dims, mc->ccells, COARSE_CELL, r, 0.0, INFINITY, &f->coarse);
 }
 
+/* debug tracing of one (pixel, sample): SO_TRACE="x,y,s" */
+
+static int flight_next_impl(flight_t* f, int cell[3], double* ta, double* tb);
 static int flight_next(flight_t* f, int cell[3], double* ta, double* tb)
+{
+    if (g_trace) {
+        int r = flight_next_impl(f, cell, ta, tb);
+        if (r) fprintf(stderr, "[oracle] visit %d %d %d %a %a\n", cell[0], cell[1], cell[2], *ta, *tb);
+        else fprintf(stderr, "[oracle] flight end\n");
+        return r;
+    }
+    return flight_next_impl(f, cell, ta, tb);
+}
+
+static int flight_next_impl(flight_t* f, int cell[3], double* ta, double* tb)
 {
     const mc_t* mc = f->mc;
     if (!mc->cdraw)
@@ -549,6 +567,7 @@ static int flight_next(flight_t* f, int cell[3], double* ta, double* tb)
         int cc[3];
         double a, b;
         if (!dda_next_cells(mc->ccells, &f->coarse, cc, &a, &b)) return 0;
+        if (g_trace) fprintf(stderr, "[oracle] region %d %d %d %a %a\n", cc[0], cc[1], cc[2], a, b);
         if (!mc->cdraw[(size_t)cc[0] + (size_t)mc->ccells[0] * ((size_t)cc[1] + (size_t)mc->ccells[1] * (size_t)cc[2])])
             continue;
         if (dda_init(mc, f->ray, a, b, &f->fine)) f->in_fine = 1;
@@ -854,6 +873,12 @@ static void* render_worker(void* arg)
                 double acc3[3] = {0, 0, 0};
                 for (int sm = 0; sm < s->spp; ++sm) {
                     rng_t rng = rng_for_pixel_sample(s->seed, x, y, sm);
+                    {
+                        const char* tr = getenv("SO_TRACE");
+                        int tx = -1, ty = -1, ts = -1;
+                        if (tr) sscanf(tr, "%d,%d,%d", &tx, &ty, &ts);
+                        g_trace = x == tx && y == ty && sm == ts;
+                    }
                     double jx = rng_uniform(&rng);
                     double jy = rng_uniform(&rng);
                     ray_t ray = camera_ray(cam, (double)x + jx, (double)y + jy);

@@ -804,6 +804,12 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             Tr = 1.0;
             have = false;
         }
+#ifdef SVDB_TRACE_PIXEL
+        if (px == SVDB_TRACE_X && py == SVDB_TRACE_Y && s == SVDB_TRACE_S) {
+            const Ray rr = ray_load();
+            printf("[gpu] ray %a %a %a %a %a %a\n", rr.o[0], rr.o[1], rr.o[2], rr.d[0], rr.d[1], rr.d[2]);
+        }
+#endif
         if constexpr (HDDA) {
             if (!rdda.init(A.ccells, A.hi, ray_load(), 0.0, kInf(), 128.0, 1.0 / 128.0)) {
                 end_segment();
@@ -838,9 +844,17 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                 int rc[3];
                 double ra, rb;
                 if (!rdda.next(A.ccells, rc, ra, rb)) {
+#ifdef SVDB_TRACE_PIXEL
+                    if (px == SVDB_TRACE_X && py == SVDB_TRACE_Y && s == SVDB_TRACE_S)
+                        printf("[gpu] flight end\n");
+#endif
                     end_segment();
                     return;
                 }
+#ifdef SVDB_TRACE_PIXEL
+                if (px == SVDB_TRACE_X && py == SVDB_TRACE_Y && s == SVDB_TRACE_S)
+                    printf("[gpu] region %d %d %d %a %a\n", rc[0], rc[1], rc[2], ra, rb);
+#endif
                 if (!__ldg(A.cdraw + (rc[0] + A.ccells[0] * (rc[1] + A.ccells[1] * rc[2]))))
                     return;
                 if (!dda.init(A.cells, A.hi, ray_load(), ra, rb, A.cell, A.icell))
@@ -864,6 +878,10 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                     end_segment();
                 return;
             }
+#ifdef SVDB_TRACE_PIXEL
+            if (px == SVDB_TRACE_X && py == SVDB_TRACE_Y && s == SVDB_TRACE_S)
+                printf("[gpu] visit %d %d %d %a %a\n", c[0], c[1], c[2], ta, tbb);
+#endif
             // 1.0 / double(majorant) precomputed per cell with the same IEEE division
             // (render.hpp:113), 0 marks an empty cell. This cell's was loaded one visit ahead;
             // issue the next cell's now so the load overlaps a whole iteration.
