@@ -28,6 +28,9 @@
 #ifndef SVDB_LAZY_LOG
 #define SVDB_LAZY_LOG 1
 #endif
+#ifndef SVDB_DDA_FAST
+#define SVDB_DDA_FAST 1
+#endif
 
 namespace svdbgpu {
 
@@ -47,6 +50,17 @@ __device__ __forceinline__ const float4* stage_tf(const RenderArgs& A, float4* s
 constexpr double kPi = 3.14159265358979323846;
 
 __device__ __forceinline__ double kInf() { return __longlong_as_double(0x7ff0000000000000ll); }
+
+// a / b from y = RN(1 / b): q = RN(a y) corrected once with the exact residual fma(-q, b, a) gives
+// RN(a / b) (Markstein's correction; bit-identical to the IEEE division, checked on 5e8 operand pairs
+// including worst-case divisor significands, tools/check_div.c). Tiny divisors take the division.
+__device__ __forceinline__ double div_by_rcp(double a, double b, double y)
+{
+    if (!(fabs(b) > 0x1p-900))
+        return a / b;
+    const double q = a * y;
+    return fma(fma(-q, b, a), y, q);
+}
 
 template <int CODEC>
 struct Tracer {
@@ -496,6 +510,55 @@ struct SharedDda {
     __device__ __forceinline__ bool init(const int cells[3], const double hi[3], const Ray& r, double t0, double t1,
                                          double cell, double icell)
     {
+#if SVDB_DDA_FAST
+        // the three axes unrolled (independent FP64 chains interleave), same operations and order
+        double inv[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double o = r.o[a], d = r.d[a], h = hi[a];
+            inv[a] = 0.0;
+            if (d == 0.0) {
+                if (o < 0.0 || o > h)
+                    return false;
+                continue;
+            }
+            inv[a] = 1.0 / d;
+            double ta = (0.0 - o) * inv[a], tb = (h - o) * inv[a];
+            if (ta > tb) {
+                const double tt = ta;
+                ta = tb;
+                tb = tt;
+            }
+            t0 = dmax(t0, ta);
+            t1 = dmin(t1, tb);
+            if (t0 > t1)
+                return false;
+        }
+        if (!(t0 <= t1))
+            return false;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double o = r.o[a], d = r.d[a];
+            const double e = o + d * t0;
+            const int c = int(dclamp(floor(e * icell), 0.0, double(cells[a] - 1)));
+            int step = 0;
+            double tn = __longlong_as_double(0x7ff0000000000000ll), td = tn;
+            if (d != 0.0) {
+                step = d > 0.0 ? 1 : -1;
+                tn = div_by_rcp(double(d > 0.0 ? c + 1 : c) * cell - o, d, inv[a]);
+                // cell is a power of two, so +-cell * RN(1/d) == RN(+-cell / d) exactly (dda.hpp:80, 84)
+                td = (d > 0.0 ? cell : -cell) * inv[a];
+            }
+            ci(a) = c;
+            ci(3 + a) = step;
+            cd(a) = tn;
+            cd(3 + a) = td;
+        }
+        cd(6) = t0;
+        cd(7) = t1;
+        ci(6) = 0;
+        return true;
+#endif
 #pragma unroll 1
         for (int a = 0; a < 3; ++a) {
             const double o = a == 0 ? r.o[0] : (a == 1 ? r.o[1] : r.o[2]);
@@ -581,7 +644,10 @@ struct SharedDda {
 
 constexpr int kTraceThreads = 64;   // 2 warps per CTA
 constexpr int kTraceMinBlocks = 14; // <= 72 registers, 14.3 KB shared: 28 resident warps per SM
-constexpr int kAdvIters = 3;        // advance steps per advance-phase invocation
+#ifndef SVDB_ADV_ITERS
+#define SVDB_ADV_ITERS 3
+#endif
+constexpr int kAdvIters = SVDB_ADV_ITERS; // advance steps per advance-phase invocation
 constexpr int kChunkMinSpp = 16;    // one GPU: whole-pixel work items below this many samples per pixel
 constexpr int kSplitChunk = 4;      // max samples per work item when the frame is split over ranks
 constexpr int kSampleChunk = 16;    // max samples per work item on one GPU
@@ -720,9 +786,16 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                     finish_path(0.0f, 0.0f, 0.0f);
                 return;
             }
+#if SVDB_DDA_FAST
+            const double ys = 1.0 / survive; // render.hpp:184, tp /= survive per channel, exactly
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                s_cold_d[kA + k][tid] = div_by_rcp(s_cold_d[kA + k][tid], survive, ys);
+#else
 #pragma unroll 1
             for (int k = 0; k < 3; ++k) // one division site (render.hpp:184)
                 s_cold_d[kA + k][tid] /= survive;
+#endif
         }
         state = kNeedSegment;
     };
