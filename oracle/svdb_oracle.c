@@ -310,6 +310,53 @@ typedef struct {
 
 static inline int cell_count_axis(int d, int cd) { int n = (d - 1 + cd - 1) / cd; return n < 1 ? 1 : n; }
 
+typedef struct {
+    const so_grid* g;
+    const so_tf* tf;
+    mc_t* mc;
+    atomic_long next;
+} mc_job_t;
+
+static void mc_cell(const so_grid* g, const so_tf* tf, mc_t* mc, size_t i)
+{
+    const int cd = mc->cell;
+    int cx = (int)(i % mc->cells[0]), cy = (int)((i / mc->cells[0]) % mc->cells[1]),
+        cz = (int)(i / ((size_t)mc->cells[0] * mc->cells[1]));
+    int lo[3] = {cx * cd, cy * cd, cz * cd};
+    int c3[3] = {cx, cy, cz}, hi[3];
+    for (int a = 0; a < 3; ++a) { int h = (c3[a] + 1) * cd; hi[a] = h < g->dims[a] - 1 ? h : g->dims[a] - 1; }
+    acc_t acc = {g, NULL, NULL, NULL, 0};
+    float mn = INFINITY, mx = -INFINITY;
+    for (int z = lo[2]; z <= hi[2]; ++z)
+        for (int y = lo[1]; y <= hi[1]; ++y)
+            for (int x = lo[0]; x <= hi[0]; ++x) {
+                float v = acc_read(&acc, x, y, z);
+                mn = v < mn ? v : mn;
+                mx = mx < v ? v : mx;
+            }
+    mc->cmin[i] = mn; mc->cmax[i] = mx;
+    if (tf) {
+        double m = tf->density_scale * tf_max_alpha_in_range(tf, mn, mx);
+        mc->maj[i] = (float)m;
+        mc->empty[i] = m == 0.0 ? 1 : 0;
+    } else {
+        mc->maj[i] = 0.0f; mc->empty[i] = 1;
+    }
+}
+
+static void* mc_worker(void* arg)
+{
+    mc_job_t* J = (mc_job_t*)arg;
+    size_t nc = (size_t)J->mc->cells[0] * J->mc->cells[1] * J->mc->cells[2];
+    for (;;) {
+        long i = atomic_fetch_add(&J->next, 1);
+        if ((size_t)i >= nc) break;
+        mc_cell(J->g, J->tf, J->mc, (size_t)i);
+    }
+    return NULL;
+}
+
+/* build_macrocells + update_majorants (macrocell.hpp:74-116), cells in parallel (independent) */
 static void mc_build(const so_grid* g, const so_tf* tf, int cd, mc_t* mc)
 {
     mc->cell = cd;
@@ -317,30 +364,17 @@ static void mc_build(const so_grid* g, const so_tf* tf, int cd, mc_t* mc)
     size_t nc = (size_t)mc->cells[0] * mc->cells[1] * mc->cells[2];
     mc->cmin = (float*)malloc(nc * 4); mc->cmax = (float*)malloc(nc * 4);
     mc->maj = (float*)malloc(nc * 4); mc->empty = (uint8_t*)malloc(nc);
-    for (size_t i = 0; i < nc; ++i) {
-        int cx = (int)(i % mc->cells[0]), cy = (int)((i / mc->cells[0]) % mc->cells[1]),
-            cz = (int)(i / ((size_t)mc->cells[0] * mc->cells[1]));
-        int lo[3] = {cx * cd, cy * cd, cz * cd};
-        int c3[3] = {cx, cy, cz}, hi[3];
-        for (int a = 0; a < 3; ++a) { int h = (c3[a] + 1) * cd; hi[a] = h < g->dims[a] - 1 ? h : g->dims[a] - 1; }
-        acc_t acc = {g, NULL, NULL, NULL, 0};
-        float mn = INFINITY, mx = -INFINITY;
-        for (int z = lo[2]; z <= hi[2]; ++z)
-            for (int y = lo[1]; y <= hi[1]; ++y)
-                for (int x = lo[0]; x <= hi[0]; ++x) {
-                    float v = acc_read(&acc, x, y, z);
-                    mn = v < mn ? v : mn;
-                    mx = mx < v ? v : mx;
-                }
-        mc->cmin[i] = mn; mc->cmax[i] = mx;
-        if (tf) {
-            double m = tf->density_scale * tf_max_alpha_in_range(tf, mn, mx);
-            mc->maj[i] = (float)m;
-            mc->empty[i] = m == 0.0 ? 1 : 0;
-        } else {
-            mc->maj[i] = 0.0f; mc->empty[i] = 1;
-        }
-    }
+    mc_job_t J;
+    J.g = g; J.tf = tf; J.mc = mc;
+    atomic_init(&J.next, 0);
+    int nt = (int)sysconf(_SC_NPROCESSORS_ONLN);
+    if (nt < 1) nt = 1;
+    if ((size_t)nt > nc) nt = (int)nc;
+    if (nt > 256) nt = 256;
+    pthread_t th[256];
+    for (int i = 1; i < nt; ++i) pthread_create(&th[i], NULL, mc_worker, &J);
+    mc_worker(&J);
+    for (int i = 1; i < nt; ++i) pthread_join(th[i], NULL);
 }
 
 static void mc_free(mc_t* mc) { free(mc->cmin); free(mc->cmax); free(mc->maj); free(mc->empty); free(mc->cdraw); }

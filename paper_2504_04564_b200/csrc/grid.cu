@@ -542,6 +542,7 @@ int coarse_flags(GridImpl* g, const int ccells[3], cudaStream_t s)
 
 int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** out)
 {
+    NvtxRange nvtx("svdbgpu grid_create (validate, upload, leaf codec, apron, directory)");
     *out = nullptr;
     if (!b && n)
         return fail_code(SVDBGPU_E_INVALID_ARG, "svdb bytes are null");

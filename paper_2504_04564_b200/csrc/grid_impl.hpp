@@ -8,6 +8,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "layout.hpp"
 #include "svdbgpu.h"
@@ -16,6 +17,14 @@
 namespace svdbgpu {
 
 int cuda_fail(cudaError_t e, const char* what);
+
+// NVTX range for the host phases (visible in nsys / ncu timelines; no-op without a tool attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 #define SVDB_CUDA(call)                                                                        \
     do {                                                                                       \

@@ -190,6 +190,7 @@ extern "C" int svdbgpu_render_multi(svdbgpu_grid* const* grids, int32_t ndev, co
             if (rcs[size_t(k)])
                 return fail_code(rcs[size_t(k)], "device " + std::to_string(devs[size_t(k)]) + ": " + errs[size_t(k)]);
         // 2. the one collective: packed tiles of devices 1..n-1 -> slots 1..n-1 on device 0
+        NvtxRange nvtx("svdbgpu_render_multi NCCL gather");
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         SVDB_CUDA(cudaSetDevice(g0->device));
         SVDB_CUDA(cudaEventCreate(&e0));

@@ -29,7 +29,10 @@
 #define SVDB_LAZY_LOG 1
 #endif
 #ifndef SVDB_DDA_FAST
-#define SVDB_DDA_FAST 1
+#define SVDB_DDA_FAST 0 // A/B: 1 unrolled init + corrected divisions, 2 rolled + corrected, 3 unrolled plain
+#endif
+#ifndef SVDB_RR_RCP
+#define SVDB_RR_RCP 0
 #endif
 
 namespace svdbgpu {
@@ -510,7 +513,7 @@ struct SharedDda {
     __device__ __forceinline__ bool init(const int cells[3], const double hi[3], const Ray& r, double t0, double t1,
                                          double cell, double icell)
     {
-#if SVDB_DDA_FAST
+#if SVDB_DDA_FAST == 1 || SVDB_DDA_FAST == 3
         // the three axes unrolled (independent FP64 chains interleave), same operations and order
         double inv[3];
 #pragma unroll
@@ -545,7 +548,11 @@ struct SharedDda {
             double tn = __longlong_as_double(0x7ff0000000000000ll), td = tn;
             if (d != 0.0) {
                 step = d > 0.0 ? 1 : -1;
+#if SVDB_DDA_FAST == 1
                 tn = div_by_rcp(double(d > 0.0 ? c + 1 : c) * cell - o, d, inv[a]);
+#else
+                tn = (double(d > 0.0 ? c + 1 : c) * cell - o) / d;
+#endif
                 // cell is a power of two, so +-cell * RN(1/d) == RN(+-cell / d) exactly (dda.hpp:80, 84)
                 td = (d > 0.0 ? cell : -cell) * inv[a];
             }
@@ -595,7 +602,11 @@ struct SharedDda {
             double tn = __longlong_as_double(0x7ff0000000000000ll), td = tn;
             if (d != 0.0) {
                 step = d > 0.0 ? 1 : -1;
+#if SVDB_DDA_FAST == 2
+                tn = div_by_rcp(double(d > 0.0 ? c + 1 : c) * cell - o, d, cd(3 + a));
+#else
                 tn = (double(d > 0.0 ? c + 1 : c) * cell - o) / d;
+#endif
                 // cell is a power of two, so +-cell * RN(1/d) == RN(+-cell / d) exactly (dda.hpp:80, 84)
                 td = (d > 0.0 ? cell : -cell) * cd(3 + a);
             }
@@ -786,7 +797,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                     finish_path(0.0f, 0.0f, 0.0f);
                 return;
             }
-#if SVDB_DDA_FAST
+#if SVDB_RR_RCP
             const double ys = 1.0 / survive; // render.hpp:184, tp /= survive per channel, exactly
 #pragma unroll
             for (int k = 0; k < 3; ++k)
@@ -1283,6 +1294,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         return fail_code(SVDBGPU_E_UNSUPPORTED, "FP32 tracking is implemented for the pathtrace and ratio "
                                                 "integrators of the path-regenerating kernel");
     SVDB_CUDA(cudaSetDevice(g->device));
+    NvtxRange nvtx("svdbgpu render");
     RenderArgs A{};
     if (int rc = g->upload_tf(tf, s, &A.tf))
         return rc;

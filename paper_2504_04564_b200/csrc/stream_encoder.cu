@@ -409,6 +409,7 @@ int grid_for(long long n, int threads = 256) { return int(std::min<long long>((n
 int encode(SlabSource& src, const int32_t dims[3], int voxel_type, double quality, int metric, HostBuf& out,
            svdbgpu_compress_report* rep)
 {
+    NvtxRange nvtx("svdbgpu streaming encoder");
     const int dx = dims[0], dy = dims[1], dz = dims[2];
     const long long slab_vox = (long long)dx * dy * kSlab;
     const int nslabs = (dz + kSlab - 1) / kSlab;
