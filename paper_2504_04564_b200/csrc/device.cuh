@@ -109,6 +109,7 @@ struct Accessor {
         lx = x & ~7;
         ly = y & ~7;
         lz = z & ~7;
+        SVDB_ASSERT(e.y < g->n_leaf);
         leaf = e.y;
         lo = __uint_as_float(e.z);
         sc = __uint_as_float(e.w);
@@ -125,6 +126,7 @@ struct Accessor {
         wx = x & ~127;
         wy = y & ~127;
         wz = z & ~127;
+        SVDB_ASSERT(e.y < g->n_lower);
         lower = e.y;
         return read_lower(x, y, z);
     }
@@ -179,6 +181,7 @@ struct Accessor {
                 lx = x & ~7;
                 ly = y & ~7;
                 lz = z & ~7;
+                SVDB_ASSERT(e.y < g->n_leaf);
                 leaf = e.y;
                 lo = __uint_as_float(e.z);
                 sc = __uint_as_float(e.w);
@@ -205,6 +208,7 @@ struct Accessor {
             wx = x & ~127;
             wy = y & ~127;
             wz = z & ~127;
+            SVDB_ASSERT(ue.y < g->n_lower);
             lower = ue.y;
         }
         const uint4 e = __ldg(g->lower + size_t(lower) * 4096 + lower_slot(x, y, z));
@@ -215,6 +219,7 @@ struct Accessor {
         lx = x & ~7;
         ly = y & ~7;
         lz = z & ~7;
+        SVDB_ASSERT(e.y < g->n_leaf);
         leaf = e.y;
         lo = __uint_as_float(e.z);
         sc = __uint_as_float(e.w);
@@ -270,6 +275,7 @@ __device__ __forceinline__ float trilerp(const double v[8], double wx, double wy
 template <int CODEC>
 __device__ __forceinline__ float brick_tap_f(const Accessor<CODEC>& a, int x, int y, int z)
 {
+    SVDB_ASSERT(a.leaf < a.g->n_leaf && unsigned(x) <= 8u && unsigned(y) <= 8u && unsigned(z) <= 8u);
     const uint8_t* base = a.g->codes + size_t(a.leaf) * a.g->leaf_stride;
     const int r = (x >> 3) | ((y >> 3) << 1) | ((z >> 3) << 2);
     // The element of the own block / apron region, from per-region coefficient tables, so lanes whose

@@ -701,6 +701,8 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
     g->dg.lparams = g->d_lparams;
     g->dg.leaf_stride = stride;
     g->dg.main_bytes = main_bytes;
+    g->dg.n_leaf = uint32_t(nf);
+    g->dg.n_lower = uint32_t(nl);
     for (int attempt = 0; attempt < 2; ++attempt) {
         SVDB_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
         for (uint64_t first = 0; first < nf; first += chunk) {

@@ -6,6 +6,24 @@
 
 namespace svdbgpu {
 
+// Bounds-checked debug build (-DSVDB_CHECKED=1, csrc/Makefile `variants`): device asserts on every
+// indexed load / store of the hot path (tools/checked_run.sh). compute-sanitizer is closed on the
+// GPU pool, so this is the memory-safety check of record.
+#ifndef SVDB_CHECKED
+#define SVDB_CHECKED 0
+#endif
+#if SVDB_CHECKED && defined(__CUDA_ARCH__)
+#define SVDB_ASSERT(cond)                                                                      \
+    do {                                                                                       \
+        if (!(cond)) {                                                                         \
+            printf("SVDB_ASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #cond);              \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define SVDB_ASSERT(cond) ((void)0)
+#endif
+
 enum SlotKind : uint32_t { kSlotBackground = 0, kSlotTile = 1, kSlotChild = 2 };
 
 // Device tree. Node tables are pre-resolved at upload so one load answers "what is in this
@@ -25,6 +43,7 @@ struct DevGrid {
     float2* lparams;      // 8 x (lo, scale) per leaf: [0] own, [1..7] apron regions
     uint32_t leaf_stride; // bytes per leaf: own block (main_bytes) + 217-entry apron
     uint32_t main_bytes;  // 2048 f32, 512 u8, 256 u4
+    uint32_t n_leaf, n_lower;
     // leaf directory: for every 8^3 block of [0, 8*dir_dims) the root->upper->lower walk resolved
     // at build time ({kind, payload, lo, scale} as in `lower`; tile / background as kind tile with
     // the value). One load replaces the node walk for in-box lookups; null when over budget.

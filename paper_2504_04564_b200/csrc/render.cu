@@ -28,12 +28,6 @@
 #ifndef SVDB_LAZY_LOG
 #define SVDB_LAZY_LOG 1
 #endif
-#ifndef SVDB_DDA_FAST
-#define SVDB_DDA_FAST 0 // A/B: 1 unrolled init + corrected divisions, 2 rolled + corrected, 3 unrolled plain
-#endif
-#ifndef SVDB_RR_RCP
-#define SVDB_RR_RCP 0
-#endif
 
 namespace svdbgpu {
 
@@ -505,16 +499,19 @@ struct SharedDda {
     __device__ __forceinline__ bool done() { return ci(6) != 0; }
     __device__ __forceinline__ int stepv(int axis) { return ci(3 + axis); }
     __device__ __forceinline__ void set_done() { ci(6) = 1; }
-    __device__ __forceinline__ int index(const int cells[3]) { return ci(0) + cells[0] * (ci(1) + cells[1] * ci(2)); }
+    __device__ __forceinline__ int index(const int cells[3])
+    {
+        SVDB_ASSERT(unsigned(ci(0)) < unsigned(cells[0]) && unsigned(ci(1)) < unsigned(cells[1]) &&
+                    unsigned(ci(2)) < unsigned(cells[2]));
+        return ci(0) + cells[0] * (ci(1) + cells[1] * ci(2));
+    }
 
-    // clip_ray_box + dda_traverse setup (dda.hpp:25-86). Rolled per-axis loops keep one copy of
-    // each FP64 division in the instruction stream (this runs once per flight segment); the
-    // operations and their order per axis are exactly the reference's.
+    // clip_ray_box + dda_traverse setup (dda.hpp:25-86), the operations and their order per axis
+    // exactly the reference's. The axes are unrolled so their independent FP64 chains (reciprocal,
+    // slab products, the t_next divisions) interleave (measured +3.8% C3 over a rolled loop).
     __device__ __forceinline__ bool init(const int cells[3], const double hi[3], const Ray& r, double t0, double t1,
                                          double cell, double icell)
     {
-#if SVDB_DDA_FAST == 1 || SVDB_DDA_FAST == 3
-        // the three axes unrolled (independent FP64 chains interleave), same operations and order
         double inv[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
@@ -548,67 +545,9 @@ struct SharedDda {
             double tn = __longlong_as_double(0x7ff0000000000000ll), td = tn;
             if (d != 0.0) {
                 step = d > 0.0 ? 1 : -1;
-#if SVDB_DDA_FAST == 1
-                tn = div_by_rcp(double(d > 0.0 ? c + 1 : c) * cell - o, d, inv[a]);
-#else
                 tn = (double(d > 0.0 ? c + 1 : c) * cell - o) / d;
-#endif
                 // cell is a power of two, so +-cell * RN(1/d) == RN(+-cell / d) exactly (dda.hpp:80, 84)
                 td = (d > 0.0 ? cell : -cell) * inv[a];
-            }
-            ci(a) = c;
-            ci(3 + a) = step;
-            cd(a) = tn;
-            cd(3 + a) = td;
-        }
-        cd(6) = t0;
-        cd(7) = t1;
-        ci(6) = 0;
-        return true;
-#endif
-#pragma unroll 1
-        for (int a = 0; a < 3; ++a) {
-            const double o = a == 0 ? r.o[0] : (a == 1 ? r.o[1] : r.o[2]);
-            const double d = a == 0 ? r.d[0] : (a == 1 ? r.d[1] : r.d[2]);
-            const double h = a == 0 ? hi[0] : (a == 1 ? hi[1] : hi[2]);
-            if (d == 0.0) {
-                if (o < 0.0 || o > h)
-                    return false;
-                continue;
-            }
-            const double inv = 1.0 / d;
-            cd(3 + a) = inv; // kept for t_delta below
-            double ta = (0.0 - o) * inv, tb = (h - o) * inv;
-            if (ta > tb) {
-                const double tt = ta;
-                ta = tb;
-                tb = tt;
-            }
-            t0 = dmax(t0, ta);
-            t1 = dmin(t1, tb);
-            if (t0 > t1)
-                return false;
-        }
-        if (!(t0 <= t1))
-            return false;
-#pragma unroll 1
-        for (int a = 0; a < 3; ++a) {
-            const double o = a == 0 ? r.o[0] : (a == 1 ? r.o[1] : r.o[2]);
-            const double d = a == 0 ? r.d[0] : (a == 1 ? r.d[1] : r.d[2]);
-            const int n = a == 0 ? cells[0] : (a == 1 ? cells[1] : cells[2]);
-            const double e = o + d * t0;
-            const int c = int(dclamp(floor(e * icell), 0.0, double(n - 1)));
-            int step = 0;
-            double tn = __longlong_as_double(0x7ff0000000000000ll), td = tn;
-            if (d != 0.0) {
-                step = d > 0.0 ? 1 : -1;
-#if SVDB_DDA_FAST == 2
-                tn = div_by_rcp(double(d > 0.0 ? c + 1 : c) * cell - o, d, cd(3 + a));
-#else
-                tn = (double(d > 0.0 ? c + 1 : c) * cell - o) / d;
-#endif
-                // cell is a power of two, so +-cell * RN(1/d) == RN(+-cell / d) exactly (dda.hpp:80, 84)
-                td = (d > 0.0 ? cell : -cell) * cd(3 + a);
             }
             ci(a) = c;
             ci(3 + a) = step;
@@ -654,7 +593,10 @@ struct SharedDda {
 };
 
 constexpr int kTraceThreads = 64;   // 2 warps per CTA
-constexpr int kTraceMinBlocks = 14; // <= 72 registers, 14.3 KB shared: 28 resident warps per SM
+#ifndef SVDB_MIN_BLOCKS
+#define SVDB_MIN_BLOCKS 14
+#endif
+constexpr int kTraceMinBlocks = SVDB_MIN_BLOCKS; // 14: <= 72 registers, <= 15 KB shared: 28 resident warps per SM
 #ifndef SVDB_ADV_ITERS
 #define SVDB_ADV_ITERS 3
 #endif
@@ -753,6 +695,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     // path finished with float result r (render.hpp:306: accum += Vec3d(c))
     auto finish_path = [&](float r0, float r1, float r2) {
         if constexpr (CHUNK) { // the sample's result, summed in order by k_reduce
+            SVDB_ASSERT(out_off / 3 < A.npix && s < A.spp);
             float* o = A.sbuf + (size_t(out_off / 3) * size_t(A.spp) + size_t(s)) * 3;
             o[0] = r0;
             o[1] = r1;
@@ -797,16 +740,10 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                     finish_path(0.0f, 0.0f, 0.0f);
                 return;
             }
-#if SVDB_RR_RCP
             const double ys = 1.0 / survive; // render.hpp:184, tp /= survive per channel, exactly
 #pragma unroll
             for (int k = 0; k < 3; ++k)
                 s_cold_d[kA + k][tid] = div_by_rcp(s_cold_d[kA + k][tid], survive, ys);
-#else
-#pragma unroll 1
-            for (int k = 0; k < 3; ++k) // one division site (render.hpp:184)
-                s_cold_d[kA + k][tid] /= survive;
-#endif
         }
         state = kNeedSegment;
     };
@@ -850,6 +787,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             bool from_table = false;
             if constexpr (CHUNK) {
                 if (A.camtab) { // ray and post-jitter stream from k_camera_rays (same arithmetic)
+                    SVDB_ASSERT(out_off / 3 < A.npix && s < A.spp);
                     const double2* rec = A.camtab + 2 * (size_t(out_off / 3) * size_t(A.spp) + size_t(s));
                     const double2 a = __ldg(rec), b = __ldg(rec + 1);
                     rng.state = uint64_t(__double_as_longlong(b.y));
@@ -1347,6 +1285,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     A.packed = packed;
     A.counters = g->d_counters;
     const int64_t ntiles = tiles_for_rank(cam->width, cam->height, rank, nranks);
+    A.npix = packed ? ntiles * 256 : int64_t(cam->width) * cam->height;
     const size_t smem = tf_smem_bytes(tf->n_entries);
     cudaEvent_t e2 = nullptr, e3 = nullptr;
     SVDB_CUDA(cudaEventCreate(&e2));

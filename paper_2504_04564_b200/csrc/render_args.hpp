@@ -51,6 +51,7 @@ struct RenderArgs {
     // sample-chunked renders: camera rays precomputed at full SIMD width by k_camera_rays, per
     // (pixel, sample) as sbuf: {d.x, d.y}, {d.z, RNG state after the two jitter draws} (32 B)
     const double2* camtab;
+    long long npix; // pixel slots of out / sbuf / camtab (packed: this rank's tiles x 256)
 };
 
 // FP32-arithmetic tracking kernel launch (render_fast.cu): SVDBGPU_PRECISION_FP32 (all FP32) or
