@@ -276,16 +276,25 @@ class CpuReference:
                                                 tile_phase=phase % stride, threads=threads, rgb=rgb, count=count)
         return rgb, lk, pa, sec
 
+    def spread(self, stride):
+        """A stride coprime to the tile row length, so a subset samples every column of the frame."""
+        import math
+        tx = (self.cam.width + 15) // 16
+        stride = max(1, min(stride, self.tiles))
+        while stride > 1 and math.gcd(stride, tx) != 1:
+            stride += 1
+        return stride
+
     def stride_for(self, seconds, threads=0, start=64):
         """Tile stride whose pass takes about `seconds` (calibrated on a 1/start sample)."""
-        st = max(1, min(start, self.tiles))
+        st = self.spread(start)
         _, _, pa, sec = self.pass_(st, st - 1, threads=threads)
         rate = pa / max(sec, 1e-6)
         paths_frame = self.cam.width * self.cam.height * self.sc.settings.spp
-        return max(1, min(self.tiles, int(round(paths_frame / max(rate * seconds, 1.0)))))
+        return self.spread(int(round(paths_frame / max(rate * seconds, 1.0))))
 
     def lookups_per_path(self):
-        st = max(1, self.tiles // 64)
+        st = self.spread(max(1, self.tiles // 64))
         _, lk, pa, _ = self.pass_(st, 0, count=True)
         return lk / max(pa, 1)
 

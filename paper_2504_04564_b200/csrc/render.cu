@@ -28,6 +28,9 @@
 #ifndef SVDB_LAZY_LOG
 #define SVDB_LAZY_LOG 1
 #endif
+#ifndef SVDB_DEFER_ESCAPE
+#define SVDB_DEFER_ESCAPE 1
+#endif
 
 namespace svdbgpu {
 
@@ -481,7 +484,13 @@ __global__ void __launch_bounds__(256) k_render(const __grid_constant__ RenderAr
 // boundary); the grid is sized to the resident CTA count.
 enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4, kPoint = 5, kScatter = 6,
              kNeedRegion = 7, // hierarchical DDA: next 128^3 lower-node region
-             kNeedLog = 8 };  // tentative step whose cell-exit decision needs the exact FP64 log
+             kNeedLog = 8,    // tentative step whose cell-exit decision needs the exact FP64 log
+             kEscape = 9 };   // flight over (left the grid / Tr = 0): result written in the start phase
+// the phase each state waits for, 2 bits per state: 0 start, 1 advance, 2 gather, 3 none (kNeedPixel)
+constexpr uint32_t kPhaseOf = (3u << 2 * kNeedPixel) | (0u << 2 * kNeedPath) | (0u << 2 * kNeedSegment) |
+                              (1u << 2 * kNeedCell) | (1u << 2 * kInCell) | (2u << 2 * kPoint) | (0u << 2 * kScatter) |
+                              (1u << 2 * kNeedRegion) | (2u << 2 * kNeedLog) | (0u << 2 * kEscape);
+__device__ __forceinline__ int phase_of(int state) { return int(kPhaseOf >> (2 * state)) & 3; }
 
 // The macrocell DDA of device.cuh (dda.hpp:52-109), same arithmetic, with its 23 words of
 // per-lane state in shared memory (SoA, conflict-free) instead of registers: it is touched once
@@ -762,9 +771,22 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                         float(tp2 * double(A.ambient[2])));
         }
     };
-    // kScatter / kNeedPath / kNeedSegment: scatter, write a finished pixel, start the next sample
-    // (render.hpp:298-302), or enter the macrocell DDA with a new flight (render.hpp:142)
+    // a flight that ran out of cells (or of transmittance) ends in the start phase, batched with
+    // the other lanes writing results and starting paths, instead of inside the advance / gather
+    // iteration where it ran with a lane or two
+    auto flight_over = [&]() {
+#if SVDB_DEFER_ESCAPE
+        state = kEscape;
+#else
+        end_segment();
+#endif
+    };
+    // kEscape / kScatter / kNeedPath / kNeedSegment: finish a flight, scatter, write a finished pixel,
+    // start the next sample (render.hpp:298-302), or enter the macrocell DDA with a new flight
+    // (render.hpp:142)
     auto do_start = [&]() {
+        if (state == kEscape)
+            end_segment();
         if (state == kScatter) { // the only copy of the scattering code in the loop
             bounce(t_ev, v_ev);
             if (state == kNeedSegment)
@@ -870,7 +892,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                     if (px == SVDB_TRACE_X && py == SVDB_TRACE_Y && s == SVDB_TRACE_S)
                         printf("[gpu] flight end\n");
 #endif
-                    end_segment();
+                    flight_over();
                     return;
                 }
 #ifdef SVDB_TRACE_PIXEL
@@ -890,14 +912,14 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             int c[3];
             double ta, tbb;
             if (RATIO && !(Tr > 0.0)) {
-                end_segment();
+                flight_over();
                 return;
             }
             if (!dda.next(A.cells, c, ta, tbb)) {
                 if constexpr (HDDA)
                     state = kNeedRegion; // the region's majorant cells are done
                 else
-                    end_segment();
+                    flight_over();
                 return;
             }
 #ifdef SVDB_TRACE_PIXEL
@@ -952,7 +974,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             }
             Tr *= 1.0 - r;
             if (!(Tr > 0.0))
-                end_segment();
+                flight_over();
             else
                 state = kInCell;
         } else {
@@ -1029,9 +1051,10 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             continue; // finished lanes idle until the whole warp is done
         // ---- phase selection: run the one phase most lanes are waiting in; ties go to the
         // gather so its memory latency is paid by as many lanes as possible at once ----
-        const int nS = __popc(__ballot_sync(live, state == kPoint || state == kNeedLog));
-        const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell || state == kNeedRegion));
-        const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter));
+        const int ph = phase_of(state);
+        const int nS = __popc(__ballot_sync(live, ph == 2));
+        const int nA = __popc(__ballot_sync(live, ph == 1));
+        const int nT = __popc(__ballot_sync(live, ph == 0));
         const int phase = (nS > 0 && nS >= nA && nS >= nT) || (nA == 0 && nT == 0) ? 2 : (nA >= nT ? 1 : 0);
 #ifdef SVDB_PHASE_STATS
         if (lane == __ffs(live) - 1) { // per phase: invocations and participating lanes
@@ -1041,11 +1064,11 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         }
 #endif
         if (phase == 0) {
-            if (state == kNeedPath || state == kNeedSegment || state == kScatter)
+            if (ph == 0)
                 do_start();
         } else if (phase == 1) {
 #pragma unroll 1
-            for (int k = 0; k < kAdvIters && (state == kNeedCell || state == kInCell || state == kNeedRegion); ++k)
+            for (int k = 0; k < kAdvIters && phase_of(state) == 1; ++k)
                 do_advance();
         } else {
             if (state == kNeedLog)
