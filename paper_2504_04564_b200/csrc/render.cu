@@ -486,11 +486,6 @@ enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kIn
              kNeedRegion = 7, // hierarchical DDA: next 128^3 lower-node region
              kNeedLog = 8,    // tentative step whose cell-exit decision needs the exact FP64 log
              kEscape = 9 };   // flight over (left the grid / Tr = 0): result written in the start phase
-// the phase each state waits for, 2 bits per state: 0 start, 1 advance, 2 gather, 3 none (kNeedPixel)
-constexpr uint32_t kPhaseOf = (3u << 2 * kNeedPixel) | (0u << 2 * kNeedPath) | (0u << 2 * kNeedSegment) |
-                              (1u << 2 * kNeedCell) | (1u << 2 * kInCell) | (2u << 2 * kPoint) | (0u << 2 * kScatter) |
-                              (1u << 2 * kNeedRegion) | (2u << 2 * kNeedLog) | (0u << 2 * kEscape);
-__device__ __forceinline__ int phase_of(int state) { return int(kPhaseOf >> (2 * state)) & 3; }
 
 // The macrocell DDA of device.cuh (dda.hpp:52-109), same arithmetic, with its 23 words of
 // per-lane state in shared memory (SoA, conflict-free) instead of registers: it is touched once
@@ -1051,10 +1046,10 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             continue; // finished lanes idle until the whole warp is done
         // ---- phase selection: run the one phase most lanes are waiting in; ties go to the
         // gather so its memory latency is paid by as many lanes as possible at once ----
-        const int ph = phase_of(state);
-        const int nS = __popc(__ballot_sync(live, ph == 2));
-        const int nA = __popc(__ballot_sync(live, ph == 1));
-        const int nT = __popc(__ballot_sync(live, ph == 0));
+        const int nS = __popc(__ballot_sync(live, state == kPoint || state == kNeedLog));
+        const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell || state == kNeedRegion));
+        const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter ||
+                                                      state == kEscape));
         const int phase = (nS > 0 && nS >= nA && nS >= nT) || (nA == 0 && nT == 0) ? 2 : (nA >= nT ? 1 : 0);
 #ifdef SVDB_PHASE_STATS
         if (lane == __ffs(live) - 1) { // per phase: invocations and participating lanes
@@ -1064,11 +1059,11 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         }
 #endif
         if (phase == 0) {
-            if (ph == 0)
+            if (state == kNeedPath || state == kNeedSegment || state == kScatter || state == kEscape)
                 do_start();
         } else if (phase == 1) {
 #pragma unroll 1
-            for (int k = 0; k < kAdvIters && phase_of(state) == 1; ++k)
+            for (int k = 0; k < kAdvIters && (state == kNeedCell || state == kInCell || state == kNeedRegion); ++k)
                 do_advance();
         } else {
             if (state == kNeedLog)
