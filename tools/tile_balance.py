@@ -12,9 +12,7 @@ from paper_2504_04564_b200 import scenes as S  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 sc = S.SCENES[name]
-vol = P.synth(sc.volume, sc.dims, sc.volume_seed, threads=0)
-svdb, _ = P.compress(vol, P.CompressionParams(1.0), voxel_type=sc.voxel_type, threads=0)
-del vol
+svdb, _, _ = P.synth_compress(sc.volume, sc.dims, sc.volume_seed)  # streaming device encoder
 g = P.DeviceGrid(svdb, sc.codec)
 cam = sc.camera()
 P.render(g, sc.tf, cam, sc.settings)  # warm-up (majorants, caches)
