@@ -422,10 +422,17 @@ class DeviceGrid:
 
 
 def render(grid: DeviceGrid, tf: TransferFunction, cam: Camera, settings: RenderSettings,
-           tile_rank: int = 0, tile_nranks: int = 1) -> Image:
+           tile_rank: int = 0, tile_nranks: int = 1, out: np.ndarray | None = None) -> Image:
     """svdb::render (render.hpp:319-325) on the GPU: macrocell ranges (cached per grid),
-    majorants for ``tf``, one path-tracing launch, image copied back to the host."""
-    rgb = np.zeros((cam.height, cam.width, 3), dtype=np.float32)
+    majorants for ``tf``, one path-tracing launch, image copied back to the host. ``out`` (optional,
+    float32 [H, W, 3], C-contiguous; e.g. a pinned buffer for a full-speed device-to-host copy)
+    receives the image instead of a new array."""
+    if out is None:
+        rgb = np.zeros((cam.height, cam.width, 3), dtype=np.float32)
+    else:
+        if out.dtype != np.float32 or out.shape != (cam.height, cam.width, 3) or not out.flags.c_contiguous:
+            raise Error(E_INVALID_ARG, "out must be a C-contiguous float32 [height, width, 3] array")
+        rgb = out
     st = N.Stats()
     ctf, ccam, cst = tf._c(), cam._c(), settings._c(tile_rank, tile_nranks)
     _check(N.lib().svdbgpu_render(grid.handle, C.byref(ctf), C.byref(ccam), C.byref(cst),
