@@ -160,6 +160,15 @@ struct Accessor {
         return read_upper(x, y, z);
     }
 
+    // read(x, y, z) through locate(): the leaf directory instead of the node walk for in-box voxels
+    __device__ __forceinline__ float read_located(int x, int y, int z)
+    {
+        float v;
+        if (locate(x, y, z, v))
+            return decode<CODEC>(*g, leaf, leaf_voxel(x, y, z), lo, sc);
+        return v;
+    }
+
     // Make the leaf holding (x,y,z) the cached leaf: no memory traffic on a leaf-cache hit, one
     // lower-slot load when the lower node is cached, the root/upper walk otherwise. Returns
     // false when (x,y,z) is not inside a leaf; `value` then holds the tile / background value
@@ -331,14 +340,27 @@ __device__ __forceinline__ float sample_trilinear(Accessor<CODEC>& a, double px,
                 v[k] = brick_tap<CODEC>(a, x + (k & 1), y + ((k >> 1) & 1), z + (k >> 2));
             return trilerp(v, wx, wy, wz);
         }
-        // base voxel in a tile / background / outside: per-tap accessor reads (rare in data
-        // regions); tap order as sample.hpp:56-63
+        // base voxel in a tile / background block (or outside the grid): a non-leaf 8^3 block has
+        // one value, so every tap inside the base block is c0 with no load; only taps across the
+        // block's far faces are looked up (through the leaf directory, independent loads). Tap
+        // order as sample.hpp:56-63.
+#ifdef SVDB_OLD_FALLBACK
         double v[8];
         v[0] = c0;
 #pragma unroll 1
         for (int i = 1; i < 8; ++i)
             v[i] = a.read(x0 + (i & 1), y0 + ((i >> 1) & 1), z0 + (i >> 2));
         return trilerp(v, wx, wy, wz);
+#else
+        const bool cx = (x0 & 7) == 7, cy = (y0 & 7) == 7, cz = (z0 & 7) == 7;
+        double v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const bool cross = ((i & 1) && cx) || (((i >> 1) & 1) && cy) || ((i >> 2) && cz);
+            v[i] = cross ? double(a.read_located(x0 + (i & 1), y0 + ((i >> 1) & 1), z0 + (i >> 2))) : double(c0);
+        }
+        return trilerp(v, wx, wy, wz);
+#endif
     }
 }
 
