@@ -344,23 +344,28 @@ __device__ __forceinline__ float sample_trilinear(Accessor<CODEC>& a, double px,
         // one value, so every tap inside the base block is c0 with no load; only taps across the
         // block's far faces are looked up (through the leaf directory, independent loads). Tap
         // order as sample.hpp:56-63.
-#ifdef SVDB_OLD_FALLBACK
-        double v[8];
-        v[0] = c0;
+        const int cross = ((x0 & 7) == 7 ? 1 : 0) | ((y0 & 7) == 7 ? 2 : 0) | ((z0 & 7) == 7 ? 4 : 0);
+        float t[8] = {c0, c0, c0, c0, c0, c0, c0, c0}; // taps are floats (sample.hpp:56-63)
+        if (cross) {
+            // one copy of the lookup in the instruction stream (rolled), results into registers
 #pragma unroll 1
-        for (int i = 1; i < 8; ++i)
-            v[i] = a.read(x0 + (i & 1), y0 + ((i >> 1) & 1), z0 + (i >> 2));
-        return trilerp(v, wx, wy, wz);
-#else
-        const bool cx = (x0 & 7) == 7, cy = (y0 & 7) == 7, cz = (z0 & 7) == 7;
-        double v[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const bool cross = ((i & 1) && cx) || (((i >> 1) & 1) && cy) || ((i >> 2) && cz);
-            v[i] = cross ? double(a.read_located(x0 + (i & 1), y0 + ((i >> 1) & 1), z0 + (i >> 2))) : double(c0);
+            for (int i = 1; i < 8; ++i) {
+                if (!(i & cross))
+                    continue;
+                const float r = a.read_located(x0 + (i & 1), y0 + ((i >> 1) & 1), z0 + (i >> 2));
+                switch (i) {
+                case 1: t[1] = r; break;
+                case 2: t[2] = r; break;
+                case 3: t[3] = r; break;
+                case 4: t[4] = r; break;
+                case 5: t[5] = r; break;
+                case 6: t[6] = r; break;
+                default: t[7] = r; break;
+                }
+            }
         }
+        const double v[8] = {t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]};
         return trilerp(v, wx, wy, wz);
-#endif
     }
 }
 
