@@ -594,6 +594,45 @@ struct SharedDda {
             cd(axis) = (axis == 0 ? n0 : (axis == 1 ? n1 : n2)) + cd(3 + axis);
         return true;
     }
+
+    // next() that also reports, from registers, whether the traversal is now over and else the
+    // linear index of the following cell (for the majorant load one visit ahead)
+    __device__ __forceinline__ bool next_ahead(const int cells[3], double& ta, double& tb, bool& over, int& ahead)
+    {
+        if (done())
+            return false;
+        const double n0 = cd(0), n1 = cd(1), n2 = cd(2), t_cur = cd(6), t1 = cd(7);
+        const bool ax1 = n1 < n0;
+        const double tm = ax1 ? n1 : n0;
+        const bool ax2 = n2 < tm;
+        const int axis = ax2 ? 2 : (ax1 ? 1 : 0);
+        const double tn = ax2 ? n2 : tm;
+        double t_exit = dmin(tn, t1);
+        t_exit = dmax(t_exit, t_cur);
+        int c0 = ci(0), c1 = ci(1), c2 = ci(2);
+        ta = t_cur;
+        tb = t_exit;
+        over = true;
+        ahead = 0;
+        if (t_exit >= t1) {
+            set_done();
+            return true;
+        }
+        cd(6) = t_exit;
+        const int c = (axis == 0 ? c0 : (axis == 1 ? c1 : c2)) + stepv(axis);
+        ci(axis) = c;
+        if (c < 0 || c >= cells[axis]) {
+            set_done();
+            return true;
+        }
+        cd(axis) = (axis == 0 ? n0 : (axis == 1 ? n1 : n2)) + cd(3 + axis);
+        c0 = axis == 0 ? c : c0;
+        c1 = axis == 1 ? c : c1;
+        c2 = axis == 2 ? c : c2;
+        over = false;
+        ahead = c0 + cells[0] * (c1 + cells[1] * c2);
+        return true;
+    }
 };
 
 constexpr int kTraceThreads = 64;   // 2 warps per CTA
@@ -904,13 +943,11 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             }
         }
         if (state == kNeedCell) {
-            int c[3];
+            // (ratio: Tr > 0 here — accept() ends the flight as soon as it reaches 0)
             double ta, tbb;
-            if (RATIO && !(Tr > 0.0)) {
-                flight_over();
-                return;
-            }
-            if (!dda.next(A.cells, c, ta, tbb)) {
+            bool over;
+            int ahead;
+            if (!dda.next_ahead(A.cells, ta, tbb, over, ahead)) {
                 if constexpr (HDDA)
                     state = kNeedRegion; // the region's majorant cells are done
                 else
@@ -919,14 +956,14 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             }
 #ifdef SVDB_TRACE_PIXEL
             if (px == SVDB_TRACE_X && py == SVDB_TRACE_Y && s == SVDB_TRACE_S)
-                printf("[gpu] visit %d %d %d %a %a\n", c[0], c[1], c[2], ta, tbb);
+                printf("[gpu] visit %a %a\n", ta, tbb);
 #endif
             // 1.0 / double(majorant) precomputed per cell with the same IEEE division
             // (render.hpp:113), 0 marks an empty cell. This cell's was loaded one visit ahead;
             // issue the next cell's now so the load overlaps a whole iteration.
             inv = inv_ahead;
-            if (!dda.done())
-                inv_ahead = __ldg(A.inv_maj + dda.index(A.cells));
+            if (!over)
+                inv_ahead = __ldg(A.inv_maj + ahead);
 #ifdef SVDB_PHASE_STATS
             ++(inv > 0.0 ? st_full : st_empty);
 #endif
@@ -1050,7 +1087,15 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell || state == kNeedRegion));
         const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter ||
                                                       state == kEscape));
-        const int phase = (nS > 0 && nS >= nA && nS >= nT) || (nA == 0 && nT == 0) ? 2 : (nA >= nT ? 1 : 0);
+        // argmax with ties to the gather, then the advance (same choice as "gather if it has the most
+        // lanes, else advance unless the start phase has more")
+        int phase = 2, best = nS;
+        if (nA > best) {
+            phase = 1;
+            best = nA;
+        }
+        if (nT > best)
+            phase = 0;
 #ifdef SVDB_PHASE_STATS
         if (lane == __ffs(live) - 1) { // per phase: invocations and participating lanes
             const int n = phase == 0 ? nT : (phase == 1 ? nA : nS);
