@@ -484,11 +484,27 @@ typedef struct {
     int c[3], step[3];
     double t_next[3], t_delta[3], t_cur, t1;
     int done;
+    int last_axis; /* axis stepped after the last visit (-1: the traversal ended there) */
+    int lo[3], hi[3]; /* cell index range walked: the grid, or one HDDA region of it */
 } dda_t;
 
+static int dda_init_forced(const int dims[3], const int cells[3], int cell, const ray_t* r, double t0, double t1,
+                           int force_axis, int force_cell, const int* clo, const int* chi, dda_t* s);
 static int dda_init_cells(const int dims[3], const int cells[3], int cell, const ray_t* r, double t0, double t1,
                           dda_t* s)
 {
+    return dda_init_forced(dims, cells, cell, r, t0, t1, -1, 0, NULL, NULL, s);
+}
+
+/* dda_init over the cell range [clo, chi] (NULL: the whole grid) with the start cell on force_axis
+   given (the hierarchical DDA's region entry face); the walk ends when it leaves the range */
+static int dda_init_forced(const int dims[3], const int cells[3], int cell, const ray_t* r, double t0, double t1,
+                           int force_axis, int force_cell, const int* clo, const int* chi, dda_t* s)
+{
+    for (int a = 0; a < 3; ++a) {
+        s->lo[a] = clo ? clo[a] : 0;
+        s->hi[a] = chi ? chi[a] : cells[a] - 1;
+    }
     double lo[3] = {0, 0, 0};
     double hi[3] = {(double)(dims[0] - 1), (double)(dims[1] - 1), (double)(dims[2] - 1)};
     if (!clip_ray_box(r, lo, hi, &t0, &t1)) return 0;
@@ -496,7 +512,7 @@ static int dda_init_cells(const int dims[3], const int cells[3], int cell, const
     double e[3], cs = (double)cell;
     ray_at(r, t0, e);
     for (int a = 0; a < 3; ++a) {
-        s->c[a] = (int)dclamp(floor(e[a] / cs), 0.0, (double)(cells[a] - 1));
+        s->c[a] = a == force_axis ? force_cell : (int)dclamp(floor(e[a] / cs), (double)s->lo[a], (double)s->hi[a]);
         s->step[a] = 0;
         s->t_next[a] = INFINITY;
         s->t_delta[a] = INFINITY;
@@ -514,6 +530,7 @@ static int dda_init_cells(const int dims[3], const int cells[3], int cell, const
     s->t_cur = t0;
     s->t1 = t1;
     s->done = 0;
+    s->last_axis = -1;
     return 1;
 }
 
@@ -534,11 +551,14 @@ static int dda_next_cells(const int cells[3], dda_t* s, int cell[3], double* ta,
     memcpy(cell, s->c, 12);
     *ta = s->t_cur;
     *tb = t_exit;
+    s->last_axis = -1;
     if (t_exit >= s->t1) { s->done = 1; return 1; }
     s->t_cur = t_exit;
     s->c[axis] += s->step[axis];
-    if (s->c[axis] < 0 || s->c[axis] >= cells[axis]) { s->done = 1; return 1; }
+    if (s->c[axis] < s->lo[axis] || s->c[axis] > s->hi[axis]) { s->done = 1; return 1; }
+    (void)cells;
     s->t_next[axis] += s->t_delta[axis];
+    s->last_axis = axis;
     return 1;
 }
 
@@ -556,6 +576,7 @@ typedef struct {
     const ray_t* ray;
     dda_t coarse, fine;
     int in_fine;
+    int entry_axis; /* face through which the next region is entered (-1: the flight's first region) */
 } flight_t;
 
 static __thread int g_trace;
@@ -567,6 +588,7 @@ static int flight_init(const mc_t* mc, const ray_t* r, flight_t* f)
     f->mc = mc;
     f->ray = r;
     f->in_fine = 0;
+    f->entry_axis = -1;
     if (!mc->cdraw) {
         f->in_fine = 1;
         return dda_init(mc, r, 0.0, INFINITY, &f->fine);
@@ -602,9 +624,25 @@ static int flight_next_impl(flight_t* f, int cell[3], double* ta, double* tb)
         double a, b;
         if (!dda_next_cells(mc->ccells, &f->coarse, cc, &a, &b)) return 0;
         if (g_trace) fprintf(stderr, "[oracle] region %d %d %d %a %a\n", cc[0], cc[1], cc[2], a, b);
+        const int ax = f->entry_axis;
+        f->entry_axis = f->coarse.last_axis;
         if (!mc->cdraw[(size_t)cc[0] + (size_t)mc->ccells[0] * ((size_t)cc[1] + (size_t)mc->ccells[1] * (size_t)cc[2])])
             continue;
-        if (dda_init(mc, f->ray, a, b, &f->fine)) f->in_fine = 1;
+        /* the entry face fixes the first majorant cell on its axis (floor of a coordinate lying on
+           the face would decide it by the last ulp of the ray) */
+        /* the region's own cells bound the majorant-grid walk (a t_next recomputed at the restart
+           may differ from the region's exit time by an ulp; stepping past the face would visit a
+           sliver of the next region's cell) */
+        const int R = COARSE_CELL / mc->cell;
+        int rlo[3], rhi[3];
+        for (int k = 0; k < 3; ++k) {
+            rlo[k] = cc[k] * R;
+            rhi[k] = (cc[k] + 1) * R < mc->cells[k] ? (cc[k] + 1) * R - 1 : mc->cells[k] - 1;
+        }
+        int fc = 0;
+        if (ax >= 0)
+            fc = f->coarse.step[ax] > 0 ? rlo[ax] : rhi[ax];
+        if (dda_init_forced(mc->dims, mc->cells, mc->cell, f->ray, a, b, ax, fc, rlo, rhi, &f->fine)) f->in_fine = 1;
     }
 }
 

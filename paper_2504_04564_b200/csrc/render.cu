@@ -514,7 +514,8 @@ struct SharedDda {
     // exactly the reference's. The axes are unrolled so their independent FP64 chains (reciprocal,
     // slab products, the t_next divisions) interleave (measured +3.8% C3 over a rolled loop).
     __device__ __forceinline__ bool init(const int cells[3], const double hi[3], const Ray& r, double t0, double t1,
-                                         double cell, double icell)
+                                         double cell, double icell, int force_axis = -1, int force_cell = 0,
+                                         const int* clo = nullptr, const int* chi = nullptr)
     {
         double inv[3];
 #pragma unroll
@@ -544,7 +545,10 @@ struct SharedDda {
         for (int a = 0; a < 3; ++a) {
             const double o = r.o[a], d = r.d[a];
             const double e = o + d * t0;
-            const int c = int(dclamp(floor(e * icell), 0.0, double(cells[a] - 1)));
+            // force_axis: the hierarchical DDA's region entry face fixes the start cell on that axis
+            const int c = a == force_axis ? force_cell
+                                          : int(dclamp(floor(e * icell), clo ? double(clo[a]) : 0.0,
+                                                       chi ? double(chi[a]) : double(cells[a] - 1)));
             int step = 0;
             double tn = __longlong_as_double(0x7ff0000000000000ll), td = tn;
             if (d != 0.0) {
@@ -595,9 +599,46 @@ struct SharedDda {
         return true;
     }
 
+    // next() that also reports the axis the traversal steps across after this visit (-1: it ended)
+    __device__ __forceinline__ bool next_axis(const int cells[3], int cell[3], double& ta, double& tb, int& stepped)
+    {
+        stepped = -1;
+        if (done())
+            return false;
+        const double n0 = cd(0), n1 = cd(1), n2 = cd(2), t_cur = cd(6), t1 = cd(7);
+        const bool ax1 = n1 < n0;
+        const double tm = ax1 ? n1 : n0;
+        const bool ax2 = n2 < tm;
+        const int axis = ax2 ? 2 : (ax1 ? 1 : 0);
+        const double tn = ax2 ? n2 : tm;
+        double t_exit = dmin(tn, t1);
+        t_exit = dmax(t_exit, t_cur);
+        cell[0] = ci(0);
+        cell[1] = ci(1);
+        cell[2] = ci(2);
+        ta = t_cur;
+        tb = t_exit;
+        if (t_exit >= t1) {
+            set_done();
+            return true;
+        }
+        cd(6) = t_exit;
+        const int c = (axis == 0 ? cell[0] : (axis == 1 ? cell[1] : cell[2])) + stepv(axis);
+        ci(axis) = c;
+        if (c < 0 || c >= cells[axis]) {
+            set_done();
+            return true;
+        }
+        cd(axis) = (axis == 0 ? n0 : (axis == 1 ? n1 : n2)) + cd(3 + axis);
+        stepped = axis;
+        return true;
+    }
+
     // next() that also reports, from registers, whether the traversal is now over and else the
     // linear index of the following cell (for the majorant load one visit ahead)
-    __device__ __forceinline__ bool next_ahead(const int cells[3], double& ta, double& tb, bool& over, int& ahead)
+    // lo / hi: the cell range walked (the grid, or the HDDA region); cells: the grid, for the index
+    __device__ __forceinline__ bool next_ahead(const int cells[3], const int lo[3], const int hi[3], double& ta,
+                                               double& tb, bool& over, int& ahead)
     {
         if (done())
             return false;
@@ -621,7 +662,9 @@ struct SharedDda {
         cd(6) = t_exit;
         const int c = (axis == 0 ? c0 : (axis == 1 ? c1 : c2)) + stepv(axis);
         ci(axis) = c;
-        if (c < 0 || c >= cells[axis]) {
+        const int lo_a = axis == 0 ? lo[0] : (axis == 1 ? lo[1] : lo[2]);
+        const int hi_a = axis == 0 ? hi[0] : (axis == 1 ? hi[1] : hi[2]);
+        if (c < lo_a || c > hi_a) {
             set_done();
             return true;
         }
@@ -689,6 +732,9 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     __shared__ int s_rdda_i[HDDA ? 7 : 1][T];
     __shared__ double s_rdda_d[HDDA ? 8 : 1][T];
     SharedDda<T> rdda{&s_rdda_i[0][0], &s_rdda_d[0][0], tid};
+    __shared__ int s_rentry[T]; // HDDA: face through which the next region is entered (-1: first region)
+    volatile int& r_entry = s_rentry[tid];
+    __shared__ int s_rrange[HDDA ? 6 : 1][T]; // HDDA: majorant-cell range of the current region
     // The step loop's live values stay in registers: t, the cell's far end tb, 1/majorant of this
     // cell and of the next one (loaded one visit ahead), the RNG state.
     double t = 0.0, tb = 0.0, inv = 0.0, inv_ahead = 0.0;
@@ -893,6 +939,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                 end_segment();
                 return;
             }
+            r_entry = -1;
             state = kNeedRegion;
             return;
         }
@@ -921,7 +968,8 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             if (state == kNeedRegion) { // next lower-node region; one without draws is skipped whole
                 int rc[3];
                 double ra, rb;
-                if (!rdda.next(A.ccells, rc, ra, rb)) {
+                int stepped;
+                if (!rdda.next_axis(A.ccells, rc, ra, rb, stepped)) {
 #ifdef SVDB_TRACE_PIXEL
                     if (px == SVDB_TRACE_X && py == SVDB_TRACE_Y && s == SVDB_TRACE_S)
                         printf("[gpu] flight end\n");
@@ -933,9 +981,26 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                 if (px == SVDB_TRACE_X && py == SVDB_TRACE_Y && s == SVDB_TRACE_S)
                     printf("[gpu] region %d %d %d %a %a\n", rc[0], rc[1], rc[2], ra, rb);
 #endif
+                const int entry = r_entry;
+                r_entry = stepped;
                 if (!__ldg(A.cdraw + (rc[0] + A.ccells[0] * (rc[1] + A.ccells[1] * rc[2]))))
                     return;
-                if (!dda.init(A.cells, A.hi, ray_load(), ra, rb, A.cell, A.icell))
+                // the region's cells bound the majorant-grid walk, and its entry face fixes the first
+                // cell on that axis (oracle flight_next)
+                const int R = 128 / int(A.cell);
+                int rlo[3], rhi[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    rlo[k] = rc[k] * R;
+                    rhi[k] = min(rlo[k] + R, A.cells[k]) - 1;
+                    s_rrange[k][tid] = rlo[k];
+                    s_rrange[3 + k][tid] = rhi[k];
+                }
+                int fc = 0;
+                if (entry >= 0)
+                    fc = rdda.stepv(entry) > 0 ? (entry == 0 ? rlo[0] : (entry == 1 ? rlo[1] : rlo[2]))
+                                               : (entry == 0 ? rhi[0] : (entry == 1 ? rhi[1] : rhi[2]));
+                if (!dda.init(A.cells, A.hi, ray_load(), ra, rb, A.cell, A.icell, entry, fc, rlo, rhi))
                     return;
                 inv_ahead = __ldg(A.inv_maj + dda.index(A.cells));
                 state = kNeedCell;
@@ -947,7 +1012,15 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             double ta, tbb;
             bool over;
             int ahead;
-            if (!dda.next_ahead(A.cells, ta, tbb, over, ahead)) {
+            int lo[3] = {0, 0, 0}, hi[3] = {A.cells[0] - 1, A.cells[1] - 1, A.cells[2] - 1};
+            if constexpr (HDDA) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    lo[k] = s_rrange[k][tid];
+                    hi[k] = s_rrange[3 + k][tid];
+                }
+            }
+            if (!dda.next_ahead(A.cells, lo, hi, ta, tbb, over, ahead)) {
                 if constexpr (HDDA)
                     state = kNeedRegion; // the region's majorant cells are done
                 else

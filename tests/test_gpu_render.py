@@ -222,16 +222,16 @@ def test_homogeneous_cube_matches_independent_mc(gpu, ref):
 def test_hdda_matches_oracle_on_multi_region_grid(gpu, orc, cell, mode):
     # hierarchical DDA (a23): 128^3 lower-node regions without draws skipped in one step, the
     # majorant grid walked inside the others. Sparse C4 field at 256^3 (8 regions) and 512^3 (64): the
-    # GPU consumes the same streams as the oracle's flight_next, visit for visit. With max_bounces 0
-    # no scatter direction is drawn, so the only libm call is the step log and frames are
-    # bit-identical; multi-bounce frames also draw sincos (CUDA vs glibc differ by <= 1 ulp, which can
-    # move a region restart by an ulp: tools/dbg_trace.py) and are held to the north-star tolerance.
+    # GPU consumes the same streams as the oracle's flight_next, visit for visit. Region entries fix
+    # the first majorant cell on the entry face's axis, so a last-ulp difference in a scattered
+    # direction (CUDA's sincos vs glibc) cannot move the restart; with max_bounces 0 no direction is
+    # drawn at all.
     for factor, imf in ((8, 32), (4, 48)):
         _, svdb, _ = scene_svdb(S.scaled("C4", factor, spp=4, image_factor=imf, mode=mode))
         g = P.DeviceGrid(svdb, P.Codec.affine8)
         deq, _, _ = orc.quantize(svdb, int(P.Codec.affine8))
         og = orc.open(deq)
-        for bounces, spp, imf2, min_same in ((0, 4, imf, 0.9999), (64, 16, imf // 2, 0.98)):
+        for bounces, spp, imf2, min_same in ((0, 4, imf, 0.9999), (64, 16, imf // 2, 0.99)):
             sc = S.scaled("C4", factor, spp=spp, image_factor=imf2, mode=mode)
             st = P.RenderSettings(spp=spp, seed=7, max_bounces=bounces, rr_start_bounce=3, mode=mode,
                                   majorant_cell=cell, hdda=1)

@@ -8,9 +8,11 @@ from paper_2504_04564_b200 import scenes as S
 from oracle.oracle import Oracle
 from helpers import scene_svdb
 x, y, s = (int(v) for v in sys.argv[1].split(","))
-sc = S.scaled("C4", 8, spp=4, image_factor=32)
+imf = int(os.environ.get("DBG_IMF", "32"))
+spp = int(os.environ.get("DBG_SPP", "4"))
+sc = S.scaled("C4", 8, spp=spp, image_factor=imf)
 _, svdb, _ = scene_svdb(sc)
-st = P.RenderSettings(spp=4, seed=7, max_bounces=64, rr_start_bounce=3, hdda=1)
+st = P.RenderSettings(spp=spp, seed=7, max_bounces=64, rr_start_bounce=3, hdda=1)
 os.environ["SO_TRACE"] = f"{x},{y},{s}"
 img, _, _ = Oracle().open(svdb).render(sc.tf, sc.camera(), st, threads=1)
 print("oracle pixel", img[y, x].tolist())
