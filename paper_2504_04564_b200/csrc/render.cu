@@ -636,7 +636,8 @@ struct SharedDda {
 
     // next() that also reports, from registers, whether the traversal is now over and else the
     // linear index of the following cell (for the majorant load one visit ahead)
-    // lo / hi: the cell range walked (the grid, or the HDDA region); cells: the grid, for the index
+    // RANGED: the walk is confined to the cell range [lo, hi] (an HDDA region), else to the grid
+    template <bool RANGED>
     __device__ __forceinline__ bool next_ahead(const int cells[3], const int lo[3], const int hi[3], double& ta,
                                                double& tb, bool& over, int& ahead)
     {
@@ -662,8 +663,8 @@ struct SharedDda {
         cd(6) = t_exit;
         const int c = (axis == 0 ? c0 : (axis == 1 ? c1 : c2)) + stepv(axis);
         ci(axis) = c;
-        const int lo_a = axis == 0 ? lo[0] : (axis == 1 ? lo[1] : lo[2]);
-        const int hi_a = axis == 0 ? hi[0] : (axis == 1 ? hi[1] : hi[2]);
+        const int lo_a = RANGED ? (axis == 0 ? lo[0] : (axis == 1 ? lo[1] : lo[2])) : 0;
+        const int hi_a = RANGED ? (axis == 0 ? hi[0] : (axis == 1 ? hi[1] : hi[2])) : cells[axis] - 1;
         if (c < lo_a || c > hi_a) {
             set_done();
             return true;
@@ -1012,7 +1013,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             double ta, tbb;
             bool over;
             int ahead;
-            int lo[3] = {0, 0, 0}, hi[3] = {A.cells[0] - 1, A.cells[1] - 1, A.cells[2] - 1};
+            int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
             if constexpr (HDDA) {
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
@@ -1020,7 +1021,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                     hi[k] = s_rrange[3 + k][tid];
                 }
             }
-            if (!dda.next_ahead(A.cells, lo, hi, ta, tbb, over, ahead)) {
+            if (!dda.template next_ahead<HDDA>(A.cells, lo, hi, ta, tbb, over, ahead)) {
                 if constexpr (HDDA)
                     state = kNeedRegion; // the region's majorant cells are done
                 else

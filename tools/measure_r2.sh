@@ -10,4 +10,4 @@ bash tools/prof.sh r2_prof_C3 > /dev/null 2>&1; echo "prof C3 rc=$?"
 bash tools/prof.sh r2_prof_C4 --config C4 > /dev/null 2>&1; echo "prof C4 rc=$?"
 bash tools/prof.sh r2_prof_C4_hdda --config C4 --hdda > /dev/null 2>&1; echo "prof C4 hdda rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sample -c 1 -o gpurun_out/r2_prof_K2 python bench.py --mode sample --steps 1 --warmup 0 > gpurun_out/r2_prof_K2.log 2>&1; echo "prof K2 rc=$?"
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2_launches_C3_bench_default.csv python bench.py --steps 2 --warmup 1 > gpurun_out/r2_launches.log 2>&1; echo "launches rc=$?"
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/r2_launches_C3_bench_default.csv python bench.py --steps 2 --warmup 1 > gpurun_out/r2_launches.log 2>&1; echo "launches rc=$?"
