@@ -25,12 +25,6 @@
 #include <cstdio>
 #include <cstring>
 
-#ifndef SVDB_LAZY_LOG
-#define SVDB_LAZY_LOG 1
-#endif
-#ifndef SVDB_DEFER_ESCAPE
-#define SVDB_DEFER_ESCAPE 1
-#endif
 
 namespace svdbgpu {
 
@@ -680,14 +674,8 @@ struct SharedDda {
 };
 
 constexpr int kTraceThreads = 64;   // 2 warps per CTA
-#ifndef SVDB_MIN_BLOCKS
-#define SVDB_MIN_BLOCKS 14
-#endif
-constexpr int kTraceMinBlocks = SVDB_MIN_BLOCKS; // 14: <= 72 registers, <= 15 KB shared: 28 resident warps per SM
-#ifndef SVDB_ADV_ITERS
-#define SVDB_ADV_ITERS 3
-#endif
-constexpr int kAdvIters = SVDB_ADV_ITERS; // advance steps per advance-phase invocation
+constexpr int kTraceMinBlocks = 14; // <= 72 registers, <= 15 KB shared: 28 resident warps per SM (16 measured slower)
+constexpr int kAdvIters = 3;        // advance steps per advance-phase invocation
 constexpr int kChunkMinSpp = 16;    // one GPU: whole-pixel work items below this many samples per pixel
 constexpr int kSplitChunk = 4;      // max samples per work item when the frame is split over ranks
 constexpr int kSampleChunk = 16;    // max samples per work item on one GPU
@@ -855,13 +843,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     // a flight that ran out of cells (or of transmittance) ends in the start phase, batched with
     // the other lanes writing results and starting paths, instead of inside the advance / gather
     // iteration where it ran with a lane or two
-    auto flight_over = [&]() {
-#if SVDB_DEFER_ESCAPE
-        state = kEscape;
-#else
-        end_segment();
-#endif
-    };
+    auto flight_over = [&]() { state = kEscape; };
     // kEscape / kScatter / kNeedPath / kNeedSegment: finish a flight, scatter, write a finished pixel,
     // start the next sample (render.hpp:298-302), or enter the macrocell DDA with a new flight
     // (render.hpp:142)
@@ -954,17 +936,13 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     // kNeedCell -> next macrocell (empty cells draw nothing, render.hpp:145-146);
     // kInCell -> one tentative step t -= ln(1-u)/sigma_maj (render.hpp:116-118)
     auto do_advance = [&]() {
-        // the step draw's log does not depend on the DDA: compute it from the next uniform before
-        // the cell lookup (independent FP64 chains interleave); the draw is consumed only if the
+        // the step draw does not depend on the DDA: its bound is computed from the next uniform
+        // before the cell lookup (independent chains interleave); the draw is consumed only if the
         // cell has draws, so the stream is unchanged
-#if SVDB_LAZY_LOG
         // a float lower bound of the step length -ln(1 - u) from the next uniform (MUFU lg2:
         // |error| <= 4e-7 (1 + y); bound taken 10x wider), computed before the cell lookup
         const float y = -__log2f(float(1.0 - rng.peek())) * 0.693147182f;
         const float y_lb = y - (4e-6f + 4e-6f * y);
-#else
-        const double lg = step_log(1.0 - rng.peek());
-#endif
         if constexpr (HDDA) {
             if (state == kNeedRegion) { // next lower-node region; one without draws is skipped whole
                 int rc[3];
@@ -1047,7 +1025,6 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             tb = tbb;
         }
         rng.skip();
-#if SVDB_LAZY_LOG
         // The step leaves the cell when t - ln(1-u) * inv >= tb, and then only that decision is
         // used, never the new t (the next non-empty cell restarts at its entry, render.hpp:113-118).
         // When the float bound already clears the gap with margin (>= 1e-6 relative, far above every
@@ -1058,10 +1035,6 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             return;
         }
         state = kNeedLog;
-#else
-        t -= lg * inv;
-        state = t >= tb ? kNeedCell : kPoint;
-#endif
     };
     // kNeedLog: the exact step with the reference's FP64 log of the draw just consumed (render.hpp:116)
     auto do_exact_step = [&]() {
