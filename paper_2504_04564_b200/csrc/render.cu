@@ -1468,7 +1468,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         if (wave) LAUNCH_T(C, SVDBGPU_MODE_RATIO) else LAUNCH_R(C, SVDBGPU_MODE_RATIO);         \
         break;                                                                                 \
     }
-        if (A.camtab && !fp32) {
+        if (A.camtab) {
             const long long n = ntiles * 256 * st->spp;
             k_camera_rays<<<unsigned(std::min<long long>((n + 255) / 256, 148LL * 32)), 256, 0, s>>>(
                 A, ntiles, g->d_camtab);
@@ -1531,7 +1531,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         stats->render_ms = rms;
         stats->macrocell_ms = double(range_ms) + double(mms);
         stats->launches = (range_ms > 0.0f ? 1u : 0u) + 1u + (hdda ? 1u : 0u) + (ntiles > 0 ? 1u : 0u) + (A.chunk ? 1u : 0u) +
-                          (A.camtab && !fp32 ? 1u : 0u);
+                          (A.camtab ? 1u : 0u);
     }
     return 0;
 }

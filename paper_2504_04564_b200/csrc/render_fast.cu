@@ -34,7 +34,8 @@ constexpr int kMinBlocksMixed = 14; // FP64 geometry: 212 B of shared state per 
 constexpr int kAdvIters = 3;       // advance steps per advance-phase invocation
 constexpr unsigned kFull = 0xffffffffu;
 
-enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4, kPoint = 5, kScatter = 6 };
+enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4, kPoint = 5, kScatter = 6,
+             kEscape = 7 }; // flight over: result written in the start phase (as render.cu's k_trace)
 
 // geometry type G: float (pure FP32) or double (FP64 ray / DDA / t, FP32 everything else)
 template <typename G>
@@ -410,7 +411,10 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
             finish_path(tp(0) * A.ambient[0], tp(1) * A.ambient[1], tp(2) * A.ambient[2]);
         }
     };
+    auto flight_over = [&]() { state = kEscape; };
     auto do_start = [&]() {
+        if (state == kEscape)
+            end_segment();
         if (state == kScatter) {
             bounce(t_ev, v_ev);
             if (state == kNeedSegment)
@@ -431,19 +435,38 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
                 state = kNeedPixel;
                 return;
             }
-            {
-                const Rng r0 = Rng::for_pixel_sample(A.seed_mixed, px, py, s);
-                rng.state = r0.state;
+            bool from_table = false;
+            if constexpr (CHUNK) {
+                if (A.camtab) { // FP64 camera ray + post-jitter stream from k_camera_rays (render.cu)
+                    const double2* rec = A.camtab + 2 * (size_t(out_off / 3) * size_t(A.spp) + size_t(s));
+                    const double2 a = __ldg(rec), b = __ldg(rec + 1);
+                    rng.state = uint64_t(__double_as_longlong(b.y));
+                    Ray r;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k)
+                        r.o[k] = G(A.cam.pos[k]);
+                    r.d[0] = G(a.x);
+                    r.d[1] = G(a.y);
+                    r.d[2] = G(b.x);
+                    ray_store(r);
+                    from_table = true;
+                }
             }
-            G jx, jy;
-            if constexpr (MIXED) {
-                jx = rng.uniform53();
-                jy = rng.uniform53();
-            } else {
-                jx = rng.uniform();
-                jy = rng.uniform();
+            if (!from_table) {
+                {
+                    const Rng r0 = Rng::for_pixel_sample(A.seed_mixed, px, py, s);
+                    rng.state = r0.state;
+                }
+                G jx, jy;
+                if constexpr (MIXED) {
+                    jx = rng.uniform53();
+                    jy = rng.uniform53();
+                } else {
+                    jx = rng.uniform();
+                    jy = rng.uniform();
+                }
+                ray_store(camera_ray_g<G>(A.cam, G(px) + jx, G(py) + jy));
             }
-            ray_store(camera_ray_g<G>(A.cam, G(px) + jx, G(py) + jy));
             tp(0) = tp(1) = tp(2) = 1.0f;
             bounces = 0;
             if constexpr (RATIO)
@@ -467,8 +490,8 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
         const float lg = __log2f(1.0f - rng.peek()); // step draw, consumed only where it is used
         if (state == kNeedCell) {
             G ta, tbb;
-            if ((RATIO && !(Tr > 0.0)) || !dda.next(A.cells, ta, tbb)) {
-                end_segment();
+            if (!dda.next(A.cells, ta, tbb)) { // (ratio: Tr > 0 here, accept() ends the flight at 0)
+                flight_over();
                 return;
             }
             inv = inv_ahead;
@@ -495,7 +518,7 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
             const double tr = Tr * (1.0 - double(r));
             Tr = tr;
             if (!(tr > 0.0f))
-                end_segment();
+                flight_over();
             else
                 state = kInCell;
         } else {
@@ -573,7 +596,8 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
         // ---- run the phase most lanes are waiting in ----
         const int nS = __popc(__ballot_sync(live, state == kPoint));
         const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell));
-        const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter));
+        const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter ||
+                                                      state == kEscape));
         if (nS >= nA && nS >= nT) {
             if (state == kPoint)
                 do_sample();
@@ -581,7 +605,7 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
 #pragma unroll 1
             for (int k = 0; k < kAdvIters && (state == kNeedCell || state == kInCell); ++k)
                 do_advance();
-        } else if (state == kNeedPath || state == kNeedSegment || state == kScatter) {
+        } else if (state == kNeedPath || state == kNeedSegment || state == kScatter || state == kEscape) {
             do_start();
         }
     }
