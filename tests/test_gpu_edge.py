@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import paper_2504_04564_b200 as P
-from helpers import SplitMix, image_parity
+from helpers import MIN_IDENTICAL, SplitMix, image_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -32,7 +32,7 @@ def _tile_grid(ref, dims=(70, 45, 33), background=0.3, seed=11):
 TF = P.TransferFunction(0.0, 1.0, [[0.9, 0.8, 0.7, 0.0], [0.6, 0.9, 0.8, 0.5], [0.9, 0.9, 0.9, 1.0]], 0.08)
 
 
-def _check(img, want, min_same=0.98):
+def _check(img, want, min_same=MIN_IDENTICAL):
     same, rmse = image_parity(img, want)
     print(f"identical {same:.4f} rel RMSE {rmse:.2e}")
     assert rmse <= RMSE_TOL and same >= min_same
@@ -146,7 +146,7 @@ def test_sample_chunked_items_match_reference(gpu, ref, spp, nranks):
         for t in range(r, tiles_x * ((cam.height + 15) // 16), nranks):
             y0, x0 = (t // tiles_x) * 16, (t % tiles_x) * 16
             full[y0:y0 + 16, x0:x0 + 16] = img[y0:y0 + 16, x0:x0 + 16]
-    _check(full, want, min_same=0.98)
+    _check(full, want)
 
 
 @pytest.mark.parametrize("spp", [4, 36])
@@ -170,7 +170,7 @@ def test_packed_device_split_and_unpack_match_reference(gpu, ref, spp):
     P.unpack_tiles_device(allp.data_ptr(), nranks, max_tiles, cam.width, cam.height, frame.data_ptr(), 0)
     torch.cuda.synchronize()
     got = frame.cpu().numpy().reshape(cam.height, cam.width, 3)
-    _check(got, want, min_same=0.98)
+    _check(got, want)
 
 
 @pytest.mark.parametrize("n_entries", [1025, 4096])

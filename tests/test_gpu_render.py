@@ -13,7 +13,7 @@ import pytest
 
 import paper_2504_04564_b200 as P
 from paper_2504_04564_b200 import scenes as S
-from helpers import image_parity, scene_svdb
+from helpers import MIN_IDENTICAL, image_parity, scene_svdb
 
 pytestmark = pytest.mark.gpu
 
@@ -44,7 +44,7 @@ def test_pathtrace_matches_reference(gpu, ref, name, factor, spp, bounces):
     same, rmse = image_parity(img.pixels, want)
     print(f"{name}: identical pixels {same:.4f}, rel RMSE {rmse:.2e}, stats {img.stats}")
     assert rmse <= RMSE_TOL
-    assert same >= 0.98
+    assert same >= MIN_IDENTICAL
     assert img.stats["paths"] == sc.width * sc.height * spp
 
 
@@ -58,7 +58,7 @@ def test_pathtrace_quantised_matches_reference_on_dequantised_grid(gpu, ref, orc
     img, want = _render_pair(lambda tf, cam, s: rg.render(tf, cam, s), g, sc)
     same, rmse = image_parity(img.pixels, want)
     print(f"{codec.name}: identical {same:.4f} rmse {rmse:.2e}")
-    assert rmse <= RMSE_TOL and same >= 0.98
+    assert rmse <= RMSE_TOL and same >= MIN_IDENTICAL
 
 
 def test_iso_matches_reference(gpu, ref):
@@ -93,7 +93,7 @@ def test_ratio_matches_oracle(gpu, orc):
     img, (want, _, _) = _render_pair(lambda tf, cam, s: og.render(tf, cam, s), g, sc)
     same, rmse = image_parity(img.pixels, want)
     print(f"ratio: identical {same:.4f} rmse {rmse:.2e}")
-    assert rmse <= RMSE_TOL and same >= 0.98
+    assert rmse <= RMSE_TOL and same >= MIN_IDENTICAL
 
 
 def test_ratio_and_delta_agree_statistically(gpu):
@@ -120,7 +120,7 @@ def test_node_majorant_grid_matches_oracle(gpu, orc, cell, mode):
     img, (want, lookups, _) = _render_pair(lambda tf, cam, s: og.render(tf, cam, s), g, sc, st)
     same, rmse = image_parity(img.pixels, want)
     print(f"cell {cell} {mode.name}: identical {same:.4f} rmse {rmse:.2e}")
-    assert rmse <= RMSE_TOL and same >= 0.98
+    assert rmse <= RMSE_TOL and same >= MIN_IDENTICAL
     if mode == P.RenderMode.pathtrace:
         assert abs(img.stats["lookups"] - lookups) <= 1e-3 * lookups
 
