@@ -678,7 +678,10 @@ constexpr int kTraceMinBlocks = 14; // <= 72 registers, <= 15 KB shared: 28 resi
 constexpr int kAdvIters = 3;        // advance steps per advance-phase invocation
 constexpr int kChunkMinSpp = 16;    // one GPU: whole-pixel work items below this many samples per pixel
 constexpr int kSplitChunk = 4;      // max samples per work item when the frame is split over ranks
-constexpr int kSampleChunk = 16;    // max samples per work item on one GPU
+#ifndef SVDB_SAMPLE_CHUNK
+#define SVDB_SAMPLE_CHUNK 16
+#endif
+constexpr int kSampleChunk = SVDB_SAMPLE_CHUNK; // max samples per work item on one GPU
 
 template <int CODEC, int MODE, bool CHUNK, bool HDDA>
 __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
