@@ -678,10 +678,7 @@ constexpr int kTraceMinBlocks = 14; // <= 72 registers, <= 15 KB shared: 28 resi
 constexpr int kAdvIters = 3;        // advance steps per advance-phase invocation
 constexpr int kChunkMinSpp = 16;    // one GPU: whole-pixel work items below this many samples per pixel
 constexpr int kSplitChunk = 4;      // max samples per work item when the frame is split over ranks
-#ifndef SVDB_SAMPLE_CHUNK
-#define SVDB_SAMPLE_CHUNK 16
-#endif
-constexpr int kSampleChunk = SVDB_SAMPLE_CHUNK; // max samples per work item on one GPU
+constexpr int kSampleChunk = 16;    // max samples per work item on one GPU (8 / 32 measured -1%)
 
 template <int CODEC, int MODE, bool CHUNK, bool HDDA>
 __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const __grid_constant__ RenderArgs A, long long n_units)
@@ -690,7 +687,6 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     const float4* s_ent = stage_tf(A, s_tf);
     constexpr unsigned FULL = 0xffffffffu;
     constexpr bool RATIO = MODE == SVDBGPU_MODE_RATIO;
-    constexpr bool EA = MODE == SVDBGPU_MODE_EA; // emission-absorption march (oracle trace_ea)
     constexpr int T = kTraceThreads;
     const int lane = threadIdx.x & 31;
     const int tid = threadIdx.x;
@@ -739,14 +735,14 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     // sample to sbuf), tp0..2, t_ev; ratio tracking adds L0..2, Tr. Names without a row of their own
     // alias the t_ev row and are written only by the initialisation below, before t_ev.
     constexpr int kA = CHUNK ? 0 : 3;
-    __shared__ double s_cold_d[kA + 4 + (RATIO ? 4 : (EA ? 2 : 0))][T];
+    __shared__ double s_cold_d[kA + 4 + (RATIO ? 4 : 0)][T];
     __shared__ int s_cold_i[6 + (RATIO ? 1 : 0) + (CHUNK ? 1 : 0)][T];
     constexpr int kAcc = CHUNK ? kA + 3 : 0;
     volatile double &acc0 = s_cold_d[kAcc][tid], &acc1 = s_cold_d[kAcc + (CHUNK ? 0 : 1)][tid],
                     &acc2 = s_cold_d[kAcc + (CHUNK ? 0 : 2)][tid];
     volatile double &tp0 = s_cold_d[kA][tid], &tp1 = s_cold_d[kA + 1][tid], &tp2 = s_cold_d[kA + 2][tid];
     volatile double& t_ev = s_cold_d[kA + 3][tid];
-    constexpr int kR0 = (RATIO || EA) ? kA + 4 : kA + 3, kR = (RATIO || EA) ? 1 : 0;
+    constexpr int kR0 = RATIO ? kA + 4 : kA + 3, kR = RATIO ? 1 : 0;
     volatile double &L0 = s_cold_d[kR0][tid], &L1 = s_cold_d[kR0 + kR][tid], &L2 = s_cold_d[kR0 + 2 * kR][tid];
     volatile double& Tr = s_cold_d[kR0 + 3 * kR][tid];
     volatile int& have_d = s_cold_i[RATIO ? 6 : 0][tid];              // ratio: event pending (0/1)
@@ -830,14 +826,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         state = kNeedSegment;
     };
     // the flight left the grid (or Tr hit 0): escape / ratio segment end
-    // EA (oracle trace_ea): C in the tp rows, the transmittance in the t_ev row, t0 / j in the L0 / L1
-    // rows, the sample index in the bounces row; t = the current sample's distance, tb = t1
     auto end_segment = [&]() {
-        if constexpr (EA) {
-            finish_path(float(tp0 + t_ev * double(A.background[0])), float(tp1 + t_ev * double(A.background[1])),
-                        float(tp2 + t_ev * double(A.background[2])));
-            return;
-        }
         if constexpr (RATIO) {
             L0 += tp0 * Tr * double(A.ambient[0]);
             L1 += tp1 * Tr * double(A.ambient[1]);
@@ -911,22 +900,6 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                 }
                 ray_store(camera_ray(A.cam, double(px) + jx, double(py) + jy));
             }
-            if constexpr (EA) {
-                // j (the third draw), clip, empty accumulation (oracle trace_ea)
-                L1 = rng.uniform();
-                tp0 = tp1 = tp2 = 0.0;
-                t_ev = 1.0;
-                double t0 = 0.0, t1 = kInf();
-                if (clip_ray_box(ray_load(), A.hi, t0, t1) && t0 <= t1) {
-                    L0 = t0;
-                    tb = t1;
-                    bounces = 0;
-                    state = kNeedCell;
-                } else {
-                    flight_over();
-                }
-                return;
-            }
             tp0 = tp1 = tp2 = 1.0;
             bounces = 0;
             if constexpr (RATIO)
@@ -963,34 +936,6 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     // kNeedCell -> next macrocell (empty cells draw nothing, render.hpp:145-146);
     // kInCell -> one tentative step t -= ln(1-u)/sigma_maj (render.hpp:116-118)
     auto do_advance = [&]() {
-        if constexpr (EA) { // next sample t0 + (k + j) dt; samples in empty macrocells are jumped over
-            const int k = bounces;
-            t = L0 + (double(k) + L1) * A.ea_step;
-            if (!(t < tb)) {
-                flight_over();
-                return;
-            }
-            const Ray ray = ray_load();
-            int c[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-                c[a] = int(dclamp(floor((ray.o[a] + ray.d[a] * t) * A.icell), 0.0, double(A.cells[a] - 1)));
-            if (__ldg(A.maj + (c[0] + A.cells[0] * (c[1] + A.cells[1] * c[2]))) == 0.0f) {
-                double te = tb;
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    if (ray.d[a] > 0.0)
-                        te = dmin(te, (double(c[a] + 1) * A.cell - ray.o[a]) / ray.d[a]);
-                    else if (ray.d[a] < 0.0)
-                        te = dmin(te, (double(c[a]) * A.cell - ray.o[a]) / ray.d[a]);
-                }
-                const double kk = floor((te - L0) / A.ea_step - L1) - 1.0;
-                bounces = (kk > double(k) ? int(kk) : k) + 1;
-                return;
-            }
-            state = kPoint;
-            return;
-        }
         // the step draw does not depend on the DDA: its bound is computed from the next uniform
         // before the cell lookup (independent chains interleave); the draw is consumed only if the
         // cell has draws, so the stream is unchanged
@@ -1125,25 +1070,6 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     // accessor state is kept between gathers: with the leaf directory a cold locate is one load.
     auto do_sample = [&]() {
         tr.acc = Accessor<CODEC>(A.g);
-        if constexpr (EA) { // one sample of the march: TF, front-to-back compositing, early out
-            const float v = tr.sample_at(ray_load(), t);
-            double rgba[4];
-            tf_lookup(A.tf, tr.ent, double(v), rgba);
-            const double a = 1.0 - exp(-(A.tf.scale * rgba[3]) * A.ea_step);
-            const double Tc = t_ev;
-            tp0 = tp0 + Tc * a * rgba[0];
-            tp1 = tp1 + Tc * a * rgba[1];
-            tp2 = tp2 + Tc * a * rgba[2];
-            const double Tn = Tc * (1.0 - a);
-            t_ev = Tn;
-            if (Tn < A.ea_min_t) {
-                flight_over();
-                return;
-            }
-            bounces = bounces + 1;
-            state = kNeedCell;
-            return;
-        }
         accept(tr.sample_at(ray_load(), t));
     };
 
@@ -1476,8 +1402,7 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
     SVDB_CUDA(cudaEventCreate(&e3));
     SVDB_CUDA(cudaEventRecord(e2, s));
     const bool wave = st->kernel != SVDBGPU_KERNEL_PER_PIXEL &&
-                      (st->mode == SVDBGPU_MODE_PATHTRACE || st->mode == SVDBGPU_MODE_RATIO ||
-                       st->mode == SVDBGPU_MODE_EA);
+                      (st->mode == SVDBGPU_MODE_PATHTRACE || st->mode == SVDBGPU_MODE_RATIO);
     // sample-chunked work items for the path-regenerating tracers: a lane renders `chunk` samples
     // of a pixel, not all spp, so the last items of a frame are short (the frame's tail shrinks
     // from ~spp to ~chunk path lengths); per-sample results go through sbuf to k_reduce
@@ -1532,23 +1457,13 @@ int render(GridImpl* g, const svdbgpu_tf* tf, const svdbgpu_camera* cam, const s
         kern<<<unsigned(blocks), kTraceThreads, smem, s>>>(A, n_units);                          \
     }
 #define LAUNCH_R(C, M) k_render<C, M><<<unsigned(ntiles), 256, smem, s>>>(A)
-#define LAUNCH_EA(C)                                                                           \
-    {                                                                                          \
-        int per_sm = 1;                                                                        \
-        auto kern = A.chunk ? k_trace<C, SVDBGPU_MODE_EA, true, false> : k_trace<C, SVDBGPU_MODE_EA, false, false>; \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTraceThreads, smem);       \
-        long long blocks = std::min<long long>((long long)std::max(per_sm, 1) * sms, (n_units * 32 + kTraceThreads - 1) / kTraceThreads); \
-        kern<<<unsigned(blocks), kTraceThreads, smem, s>>>(A, n_units);                          \
-    }
 #define BY_MODE(C)                                                                             \
     switch (st->mode) {                                                                        \
     case SVDBGPU_MODE_PATHTRACE:                                                               \
         if (wave) LAUNCH_T(C, SVDBGPU_MODE_PATHTRACE) else LAUNCH_R(C, SVDBGPU_MODE_PATHTRACE); \
         break;                                                                                 \
     case SVDBGPU_MODE_ISO: LAUNCH_R(C, SVDBGPU_MODE_ISO); break;                                \
-    case SVDBGPU_MODE_EA:                                                                      \
-        if (wave) LAUNCH_EA(C) else LAUNCH_R(C, SVDBGPU_MODE_EA);                                 \
-        break;                                                                                 \
+    case SVDBGPU_MODE_EA: LAUNCH_R(C, SVDBGPU_MODE_EA); break;                                  \
     default:                                                                                   \
         if (wave) LAUNCH_T(C, SVDBGPU_MODE_RATIO) else LAUNCH_R(C, SVDBGPU_MODE_RATIO);         \
         break;                                                                                 \
