@@ -307,9 +307,12 @@ __device__ __forceinline__ float brick_tap_f(const Accessor<CODEC>& a, int x, in
                 sc = p.y;
             }
         }
-        if constexpr (CODEC == kCodecAffine4) { // own: packed nibbles; apron: one code per byte
+        if constexpr (CODEC == kCodecAffine4) {
+            // own block: packed nibbles, the tap's nibble is x's parity (off & 1 == x & 1); apron: one
+            // code per byte, stored in both nibbles (k_build_apron), so the same shift reads it and
+            // the eight taps of a sample need two shift values, not eight
             const int bi = r ? 256 + ab + off : off >> 1;
-            const int sh = r ? 0 : (off & 1) * 4;
+            const int sh = (x & 1) * 4;
             return decode_code<CODEC>((uint32_t(__ldg(base + bi)) >> sh) & 15u, lo, sc);
         } else {
             const int e = r ? 512 + ab + off : off;
@@ -472,6 +475,15 @@ struct Rng {
         x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
         x ^= x >> 31;
         return double(x >> 11) * 0x1.0p-53;
+    }
+    // the 53 random bits of the next uniform() (u = bits * 2^-53), not consumed
+    __device__ __forceinline__ uint64_t peek_bits() const
+    {
+        uint64_t x = state + 0x9E3779B97F4A7C15ull;
+        x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+        x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+        x ^= x >> 31;
+        return x >> 11;
     }
     __device__ __forceinline__ void skip() { state += 0x9E3779B97F4A7C15ull; }
     // the value the most recent uniform() / skip() consumed (pure function of the state)

@@ -241,7 +241,8 @@ __global__ void __launch_bounds__(256) k_build_apron(DevGrid g, const int4* __re
                 ok &= q >= 0 && q <= 255 && __double2float_rn(double(q) * (1.0 / 255.0)) == cval;
                 c = uint32_t(q & 255);
             }
-            dst[e] = uint8_t(c);
+            // 4-bit: the code in both nibbles, so a tap's nibble shift depends on its x parity only
+            dst[e] = uint8_t(CODEC == kCodecAffine4 ? c * 17u : c);
         }
     }
     if (!ok)

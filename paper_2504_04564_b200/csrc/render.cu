@@ -941,7 +941,11 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         // cell has draws, so the stream is unchanged
         // a float lower bound of the step length -ln(1 - u) from the next uniform (MUFU lg2:
         // |error| <= 4e-7 (1 + y); bound taken 10x wider), computed before the cell lookup
-        const float y = -__log2f(float(1.0 - rng.peek())) * 0.693147182f;
+        // float(1 - u) from the integer draw: 1 - u = (2^53 - bits) * 2^-53 exactly, and rounding
+        // the integer to float then scaling by a power of two is the same RN(1 - u) (no FP64 ops)
+        float one_minus_u = __ull2float_rn((1ull << 53) - rng.peek_bits()) * 0x1p-53f, lg;
+        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(one_minus_u)); // normal argument (>= 2^-53)
+        const float y = -lg * 0.693147182f;
         const float y_lb = y - (4e-6f + 4e-6f * y);
         if constexpr (HDDA) {
             if (state == kNeedRegion) { // next lower-node region; one without draws is skipped whole
