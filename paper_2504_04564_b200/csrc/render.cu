@@ -655,15 +655,16 @@ struct SharedDda {
             return true;
         }
         cd(6) = t_exit;
-        const int c = (axis == 0 ? c0 : (axis == 1 ? c1 : c2)) + stepv(axis);
+        // the stepped axis' values by selects on the two comparisons (tn is already t_next[axis])
+        const int c = (ax2 ? c2 : (ax1 ? c1 : c0)) + stepv(axis);
         ci(axis) = c;
-        const int lo_a = RANGED ? (axis == 0 ? lo[0] : (axis == 1 ? lo[1] : lo[2])) : 0;
-        const int hi_a = RANGED ? (axis == 0 ? hi[0] : (axis == 1 ? hi[1] : hi[2])) : cells[axis] - 1;
+        const int lo_a = RANGED ? (ax2 ? lo[2] : (ax1 ? lo[1] : lo[0])) : 0;
+        const int hi_a = RANGED ? (ax2 ? hi[2] : (ax1 ? hi[1] : hi[0])) : cells[axis] - 1;
         if (c < lo_a || c > hi_a) {
             set_done();
             return true;
         }
-        cd(axis) = (axis == 0 ? n0 : (axis == 1 ? n1 : n2)) + cd(3 + axis);
+        cd(axis) = tn + cd(3 + axis);
         c0 = axis == 0 ? c : c0;
         c1 = axis == 1 ? c : c1;
         c2 = axis == 2 ? c : c2;
@@ -1122,10 +1123,8 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                     state = kNeedPath;
                 }
             }
-            const int take = min(__popc(need), avail);
-            fill += take;
-            for (int i = 0; i < take; ++i)
-                need &= need - 1u;
+            fill += min(__popc(need), avail);
+            need &= ~__ballot_sync(FULL, ((need >> lane) & 1u) && below < avail); // served lanes
         }
         const unsigned live = __ballot_sync(FULL, !done);
         if (live == 0)
