@@ -547,6 +547,8 @@ struct SharedDda {
             double tn = __longlong_as_double(0x7ff0000000000000ll), td = tn;
             if (d != 0.0) {
                 step = d > 0.0 ? 1 : -1;
+                // (c' cell - o) / d from the slab reciprocal RN(1/d) with one exact correction
+                // (div_by_rcp: the IEEE quotient, one reciprocal per axis instead of two divisions)
                 tn = (double(d > 0.0 ? c + 1 : c) * cell - o) / d;
                 // cell is a power of two, so +-cell * RN(1/d) == RN(+-cell / d) exactly (dda.hpp:80, 84)
                 td = (d > 0.0 ? cell : -cell) * inv[a];
@@ -628,15 +630,15 @@ struct SharedDda {
         return true;
     }
 
-    // next() that also reports, from registers, whether the traversal is now over and else the
-    // linear index of the following cell (for the majorant load one visit ahead)
+    // next() for a walk that is known not to be over (the caller keeps that in a register: the
+    // traversal has a visit left unless the previous call reported `over`), reporting whether the
+    // traversal is over after this visit and else the linear index of the following cell (for the
+    // majorant load one visit ahead); no done flag in shared memory.
     // RANGED: the walk is confined to the cell range [lo, hi] (an HDDA region), else to the grid
     template <bool RANGED>
-    __device__ __forceinline__ bool next_ahead(const int cells[3], const int lo[3], const int hi[3], double& ta,
+    __device__ __forceinline__ void next_ahead(const int cells[3], const int lo[3], const int hi[3], double& ta,
                                                double& tb, bool& over, int& ahead)
     {
-        if (done())
-            return false;
         const double n0 = cd(0), n1 = cd(1), n2 = cd(2), t_cur = cd(6), t1 = cd(7);
         const bool ax1 = n1 < n0;
         const double tm = ax1 ? n1 : n0;
@@ -650,27 +652,22 @@ struct SharedDda {
         tb = t_exit;
         over = true;
         ahead = 0;
-        if (t_exit >= t1) {
-            set_done();
-            return true;
-        }
+        if (t_exit >= t1)
+            return;
         cd(6) = t_exit;
         // the stepped axis' values by selects on the two comparisons (tn is already t_next[axis])
         const int c = (ax2 ? c2 : (ax1 ? c1 : c0)) + stepv(axis);
         ci(axis) = c;
         const int lo_a = RANGED ? (ax2 ? lo[2] : (ax1 ? lo[1] : lo[0])) : 0;
         const int hi_a = RANGED ? (ax2 ? hi[2] : (ax1 ? hi[1] : hi[0])) : cells[axis] - 1;
-        if (c < lo_a || c > hi_a) {
-            set_done();
-            return true;
-        }
+        if (c < lo_a || c > hi_a)
+            return;
         cd(axis) = tn + cd(3 + axis);
         c0 = axis == 0 ? c : c0;
         c1 = axis == 1 ? c : c1;
         c2 = axis == 2 ? c : c2;
         over = false;
         ahead = c0 + cells[0] * (c1 + cells[1] * c2);
-        return true;
     }
 };
 
@@ -993,7 +990,6 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         }
         if (state == kNeedCell) {
             // (ratio: Tr > 0 here — accept() ends the flight as soon as it reaches 0)
-            double ta, tbb;
             bool over;
             int ahead;
             int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
@@ -1004,30 +1000,30 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                     hi[k] = s_rrange[3 + k][tid];
                 }
             }
-            if (!dda.template next_ahead<HDDA>(A.cells, lo, hi, ta, tbb, over, ahead)) {
+            if (inv_ahead < 0.0) { // the walk ended with the previous visit
                 if constexpr (HDDA)
                     state = kNeedRegion; // the region's majorant cells are done
                 else
                     flight_over();
                 return;
             }
+            // t, tb of an empty cell are never read (the next non-empty visit overwrites them), so
+            // the visit's range goes straight into the step registers
+            dda.template next_ahead<HDDA>(A.cells, lo, hi, t, tb, over, ahead);
 #ifdef SVDB_TRACE_PIXEL
             if (px == SVDB_TRACE_X && py == SVDB_TRACE_Y && s == SVDB_TRACE_S)
-                printf("[gpu] visit %a %a\n", ta, tbb);
+                printf("[gpu] visit %a %a\n", t, tb);
 #endif
             // 1.0 / double(majorant) precomputed per cell with the same IEEE division
             // (render.hpp:113), 0 marks an empty cell. This cell's was loaded one visit ahead;
             // issue the next cell's now so the load overlaps a whole iteration.
             inv = inv_ahead;
-            if (!over)
-                inv_ahead = __ldg(A.inv_maj + ahead);
+            inv_ahead = over ? -1.0 : __ldg(A.inv_maj + ahead); // -1: no cell after this one
 #ifdef SVDB_PHASE_STATS
             ++(inv > 0.0 ? st_full : st_empty);
 #endif
             if (!(inv > 0.0))
                 return;
-            t = ta;
-            tb = tbb;
         }
         rng.skip();
         // The step leaves the cell when t - ln(1-u) * inv >= tb, and then only that decision is
