@@ -182,7 +182,8 @@ struct Accessor {
             const unsigned cx = unsigned(x) >> 3, cy = unsigned(y) >> 3, cz = unsigned(z) >> 3;
             if (x >= 0 && y >= 0 && z >= 0 && cx < unsigned(g->dir_dims[0]) && cy < unsigned(g->dir_dims[1]) &&
                 cz < unsigned(g->dir_dims[2])) {
-                const uint4 e = __ldg(g->dir + (size_t(cz) * unsigned(g->dir_dims[1]) + cy) * unsigned(g->dir_dims[0]) + cx);
+                // the directory has < 2^32 entries (grid.cu), so the index is 32-bit arithmetic
+                const uint4 e = __ldg(g->dir + ((cz * unsigned(g->dir_dims[1]) + cy) * unsigned(g->dir_dims[0]) + cx));
                 if (e.x != kSlotChild) {
                     value = __uint_as_float(e.y); // tile value, or the background stored as one
                     return false;
@@ -259,12 +260,9 @@ __device__ float read_voxel(const DevGrid& g, int x, int y, int z)
 // ---- sampler (sample.hpp:24-72) ----
 __device__ __forceinline__ int lattice_coord(double v)
 {
-    double f = floor(v);
-    if (f < -1.0e9)
-        return -1000000000;
-    if (f > 1.0e9)
-        return 1000000000;
-    return int(f);
+    // floor, clamped to +-1e9 (sample.hpp:24-32) without branches: the saturating conversion of
+    // floor(v) clamped in integers gives the same value for every non-NaN v
+    return min(max(__double2int_rd(v), -1000000000), 1000000000);
 }
 
 // sample.hpp:65-71: x-lerps, then y, then z, in FP64, rounded to float

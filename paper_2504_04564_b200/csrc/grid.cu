@@ -760,11 +760,13 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
     g->device_bytes = sizeof(int4) * h_root.size() + sizeof(uint2) * h_upper.size() + sizeof(uint4) * h_lower.size() +
                       uint64_t(stride) * nf + 64 * nf;
     // leaf directory over the grid's box, when it costs at most 1 GiB or no more than the lower table
+    // (and has < 2^32 entries: the device indexes it with 32-bit arithmetic)
     {
         const int3 dd = make_int3((dims[0] + 7) / 8, (dims[1] + 7) / 8, (dims[2] + 7) / 8);
         const uint64_t nd = uint64_t(dd.x) * dd.y * dd.z, bytes = nd * sizeof(uint4);
         const char* off = std::getenv("SVDBGPU_NO_LEAF_DIR"); // diagnostics: force the node walk
-        if (nd && !(off && off[0] == '1') && (bytes <= (1ull << 30) || bytes <= sizeof(uint4) * h_lower.size()) &&
+        if (nd && nd < (1ull << 32) && !(off && off[0] == '1') &&
+            (bytes <= (1ull << 30) || bytes <= sizeof(uint4) * h_lower.size()) &&
             cudaMalloc(&g->d_dir, bytes) == cudaSuccess) {
             k_build_dir<<<grid_blocks(nd), 256, 0, s>>>(g->dg, dd, g->d_dir);
             SVDB_CUDA(cudaGetLastError());
