@@ -633,13 +633,14 @@ struct SharedDda {
     // next() for a walk that is known not to be over (the caller keeps that in a register: the
     // traversal has a visit left unless the previous call reported `over`), reporting whether the
     // traversal is over after this visit and else the linear index of the following cell (for the
-    // majorant load one visit ahead); no done flag in shared memory.
+    // majorant load one visit ahead); no done flag in shared memory. The walk position t_cur is the
+    // caller's register tb (the previous visit's exit, or the entry after init), not the t_cur row.
     // RANGED: the walk is confined to the cell range [lo, hi] (an HDDA region), else to the grid
     template <bool RANGED>
     __device__ __forceinline__ void next_ahead(const int cells[3], const int lo[3], const int hi[3], double& ta,
                                                double& tb, bool& over, int& ahead)
     {
-        const double n0 = cd(0), n1 = cd(1), n2 = cd(2), t_cur = cd(6), t1 = cd(7);
+        const double n0 = cd(0), n1 = cd(1), n2 = cd(2), t_cur = tb, t1 = cd(7);
         const bool ax1 = n1 < n0;
         const double tm = ax1 ? n1 : n0;
         const bool ax2 = n2 < tm;
@@ -654,7 +655,6 @@ struct SharedDda {
         ahead = 0;
         if (t_exit >= t1)
             return;
-        cd(6) = t_exit;
         // the stepped axis' values by selects on the two comparisons (tn is already t_next[axis])
         const int c = (ax2 ? c2 : (ax1 ? c1 : c0)) + stepv(axis);
         ci(axis) = c;
@@ -928,6 +928,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             end_segment();
             return;
         }
+        tb = dda.cd(6); // the walk position (next_ahead)
         inv_ahead = __ldg(A.inv_maj + dda.index(A.cells));
         state = kNeedCell;
     };
@@ -983,6 +984,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                                                : (entry == 0 ? rhi[0] : (entry == 1 ? rhi[1] : rhi[2]));
                 if (!dda.init(A.cells, A.hi, ray_load(), ra, rb, A.cell, A.icell, entry, fc, rlo, rhi))
                     return;
+                tb = dda.cd(6);
                 inv_ahead = __ldg(A.inv_maj + dda.index(A.cells));
                 state = kNeedCell;
                 return;
@@ -1007,8 +1009,8 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                     flight_over();
                 return;
             }
-            // t, tb of an empty cell are never read (the next non-empty visit overwrites them), so
-            // the visit's range goes straight into the step registers
+            // the visit's range goes straight into the step registers: t of an empty cell is never
+            // read (the next non-empty visit overwrites it), tb carries the walk position
             dda.template next_ahead<HDDA>(A.cells, lo, hi, t, tb, over, ahead);
 #ifdef SVDB_TRACE_PIXEL
             if (px == SVDB_TRACE_X && py == SVDB_TRACE_Y && s == SVDB_TRACE_S)
