@@ -403,10 +403,11 @@ __device__ __forceinline__ void tf_lookup(const DevTF& tf, const float4* ent, do
 
 __device__ __forceinline__ double tf_alpha(const DevTF& tf, const float4* ent, double v)
 {
+    // u is in [0, n - 1] (n < 2^31): 32-bit conversions give the same index and fraction
     double u = tf_normalized(tf, v) * double(tf.n - 1);
-    unsigned long long i0 = (unsigned long long)u;
-    if ((unsigned long long)(tf.n - 2) < i0)
-        i0 = (unsigned long long)(tf.n - 2);
+    unsigned i0 = unsigned(u);
+    if (unsigned(tf.n - 2) < i0)
+        i0 = unsigned(tf.n - 2);
     double t = u - double(i0);
     return (1.0 - t) * double(ent[i0].w) + t * double(ent[i0 + 1].w);
 }

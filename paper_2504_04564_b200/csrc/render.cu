@@ -1124,17 +1124,18 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             fill += min(__popc(need), avail);
             need &= ~__ballot_sync(FULL, ((need >> lane) & 1u) && below < avail); // served lanes
         }
-        const unsigned live = __ballot_sync(FULL, !done);
-        if (live == 0)
-            break;
-        if (done)
-            continue; // finished lanes idle until the whole warp is done
         // ---- phase selection: run the one phase most lanes are waiting in; ties go to the
-        // gather so its memory latency is paid by as many lanes as possible at once ----
-        const int nS = __popc(__ballot_sync(live, state == kPoint || state == kNeedLog));
-        const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell || state == kNeedRegion));
-        const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter ||
+        // gather so its memory latency is paid by as many lanes as possible at once. Finished
+        // lanes stay in kNeedPixel, which is in no phase ----
+        const int nS = __popc(__ballot_sync(FULL, state == kPoint || state == kNeedLog));
+        const int nA = __popc(__ballot_sync(FULL, state == kNeedCell || state == kInCell || state == kNeedRegion));
+        const int nT = __popc(__ballot_sync(FULL, state == kNeedPath || state == kNeedSegment || state == kScatter ||
                                                       state == kEscape));
+        if (nS + nA + nT == 0) { // every lane waits for a work item (none left: the warp is done)
+            if (__all_sync(FULL, done))
+                break;
+            continue;
+        }
         // argmax with ties to the gather, then the advance (same choice as "gather if it has the most
         // lanes, else advance unless the start phase has more")
         int phase = 2, best = nS;
@@ -1145,7 +1146,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         if (nT > best)
             phase = 0;
 #ifdef SVDB_PHASE_STATS
-        if (lane == __ffs(live) - 1) { // per phase: invocations and participating lanes
+        if (lane == 0) { // per phase: invocations and participating lanes
             const int n = phase == 0 ? nT : (phase == 1 ? nA : nS);
             atomicAdd(A.counters + 2 + 2 * phase, 1ull);
             atomicAdd(A.counters + 3 + 2 * phase, (unsigned long long)n);
