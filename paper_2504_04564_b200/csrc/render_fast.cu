@@ -163,12 +163,11 @@ __device__ __forceinline__ RayG<G> camera_ray_g(const CamArgs& c, G px, G py)
 // Macrocell DDA (dda.hpp:25-109) in float, per-lane state in shared memory (SoA)
 template <typename G>
 struct SharedDdaG {
-    volatile int* si; // [7][kT]: c0..2, step0..2, done
+    volatile int* si; // [7][kT]: c0..2, step0..2, (unused)
     volatile G* sf;   // [8][kT]: t_next0..2, t_delta0..2, t_cur, t1
     int tid;
     __device__ __forceinline__ volatile int& ci(int k) { return si[k * kT + tid]; }
     __device__ __forceinline__ volatile G& cf(int k) { return sf[k * kT + tid]; }
-    __device__ __forceinline__ bool done() { return ci(6) != 0; }
     __device__ __forceinline__ int index(const int cells[3]) { return ci(0) + cells[0] * (ci(1) + cells[1] * ci(2)); }
 
     __device__ __forceinline__ bool init(const int cells[3], const G hi[3], const RayG<G>& r, G cell, G icell)
@@ -218,30 +217,35 @@ struct SharedDdaG {
         return true;
     }
 
-    __device__ __forceinline__ bool next(const int cells[3], G& ta, G& tb)
+    // One cell visit of a walk known not to be over (the caller's lookahead register says so),
+    // walk position in the caller's tb register; reports whether the walk is over after this
+    // visit, else the next cell's linear index (as k_trace's SharedDda::next_ahead).
+    __device__ __forceinline__ void next_ahead(const int cells[3], G& ta, G& tb, bool& over, int& ahead)
     {
-        if (ci(6))
-            return false;
-        const G n0 = cf(0), n1 = cf(1), n2 = cf(2), t_cur = cf(6), t1 = cf(7);
+        const G n0 = cf(0), n1 = cf(1), n2 = cf(2), t_cur = tb, t1 = cf(7);
         const bool ax1 = n1 < n0;
         const G tm = ax1 ? n1 : n0;
         const bool ax2 = n2 < tm;
         const int axis = ax2 ? 2 : (ax1 ? 1 : 0);
-        const G t_exit = gmax(gmin(ax2 ? n2 : tm, t1), t_cur);
+        const G tn = ax2 ? n2 : tm;
+        const G t_exit = gmax(gmin(tn, t1), t_cur);
+        int c0 = ci(0), c1 = ci(1), c2 = ci(2);
         ta = t_cur;
         tb = t_exit;
-        if (t_exit >= t1) {
-            ci(6) = 1;
-            return true;
-        }
-        cf(6) = t_exit;
-        const int c = ci(axis) + ci(3 + axis);
+        over = true;
+        ahead = 0;
+        if (t_exit >= t1)
+            return;
+        const int c = (ax2 ? c2 : (ax1 ? c1 : c0)) + ci(3 + axis);
         ci(axis) = c;
         if (c < 0 || c >= cells[axis])
-            ci(6) = 1;
-        else
-            cf(axis) = (axis == 0 ? n0 : (axis == 1 ? n1 : n2)) + cf(3 + axis);
-        return true;
+            return;
+        cf(axis) = tn + cf(3 + axis);
+        c0 = axis == 0 ? c : c0;
+        c1 = axis == 1 ? c : c1;
+        c2 = axis == 2 ? c : c2;
+        over = false;
+        ahead = c0 + cells[0] * (c1 + cells[1] * c2);
     }
 };
 
@@ -482,6 +486,7 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
             end_segment();
             return;
         }
+        tb = dda.cf(6); // the walk position (next_ahead)
         inv_ahead = __ldg(inv_tab + dda.index(A.cells));
         state = kNeedCell;
     };
@@ -489,18 +494,17 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
     auto do_advance = [&]() {
         const float lg = __log2f(1.0f - rng.peek()); // step draw, consumed only where it is used
         if (state == kNeedCell) {
-            G ta, tbb;
-            if (!dda.next(A.cells, ta, tbb)) { // (ratio: Tr > 0 here, accept() ends the flight at 0)
+            if (inv_ahead < I(0)) { // the walk ended with the previous visit (ratio: Tr > 0 here)
                 flight_over();
                 return;
             }
+            bool over;
+            int ahead;
+            dda.next_ahead(A.cells, t, tb, over, ahead); // t of an empty cell is never read
             inv = inv_ahead;
-            if (!dda.done())
-                inv_ahead = __ldg(inv_tab + dda.index(A.cells));
+            inv_ahead = over ? I(-1) : __ldg(inv_tab + ahead);
             if (!(inv > I(0)))
                 return;
-            t = ta;
-            tb = tbb;
         }
         rng.skip();
         t -= G(lg * 0.693147182f) * G(inv);
@@ -583,21 +587,19 @@ __global__ void __launch_bounds__(kT, sizeof(G) == 4 ? kMinBlocks : kMinBlocksMi
                     state = kNeedPath;
                 }
             }
-            const int take = min(__popc(need), avail);
-            fill += take;
-            for (int i = 0; i < take; ++i)
-                need &= need - 1u;
+            fill += min(__popc(need), avail);
+            need &= ~__ballot_sync(kFull, ((need >> lane) & 1u) && below < avail); // served lanes
         }
-        const unsigned live = __ballot_sync(kFull, !done);
-        if (live == 0)
-            break;
-        if (done)
+        // ---- run the phase most lanes are waiting in (finished lanes sit in kNeedPixel) ----
+        const int nS = __popc(__ballot_sync(kFull, state == kPoint));
+        const int nA = __popc(__ballot_sync(kFull, state == kNeedCell || state == kInCell));
+        const int nT = __popc(__ballot_sync(kFull, state == kNeedPath || state == kNeedSegment || state == kScatter ||
+                                                       state == kEscape));
+        if (nS + nA + nT == 0) {
+            if (__all_sync(kFull, done))
+                break;
             continue;
-        // ---- run the phase most lanes are waiting in ----
-        const int nS = __popc(__ballot_sync(live, state == kPoint));
-        const int nA = __popc(__ballot_sync(live, state == kNeedCell || state == kInCell));
-        const int nT = __popc(__ballot_sync(live, state == kNeedPath || state == kNeedSegment || state == kScatter ||
-                                                      state == kEscape));
+        }
         if (nS >= nA && nS >= nT) {
             if (state == kPoint)
                 do_sample();
