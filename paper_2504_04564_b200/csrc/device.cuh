@@ -23,9 +23,15 @@ __device__ __forceinline__ int lower_slot(int x, int y, int z)
 {
     return ((x >> 3) & 15) + 16 * (((y >> 3) & 15) + 16 * ((z >> 3) & 15));
 }
+// Leaf payload layout: the 9^3 stencil brick of the leaf, element x + 9y + 81z for brick
+// coordinates in [0, 8]: the own 8^3 block where all three are < 8, the apron (the +1 layer,
+// copied from the neighbouring blocks) where one is 8. A trilinear stencil based in the block is
+// then eight loads at fixed offsets from one element index.
+__host__ __device__ __forceinline__ int brick_index(int x, int y, int z) { return x + 9 * y + 81 * z; }
+// the own voxel (x, y, z) & 7 of a leaf
 __device__ __forceinline__ int leaf_voxel(int x, int y, int z)
 {
-    return (x & 7) + 8 * ((y & 7) + 8 * (z & 7));
+    return brick_index(x & 7, y & 7, z & 7);
 }
 
 // ---- leaf decode ----
@@ -39,7 +45,7 @@ __device__ __forceinline__ float decode_code(uint32_t c, float lo, float sc)
         return fmaf(float(c), sc, lo);
 }
 
-// voxel vi (0..511) of leaf `leaf`'s own block
+// brick element vi (leaf_voxel / brick_index) of leaf `leaf`
 template <int CODEC>
 __device__ __forceinline__ float decode(const DevGrid& g, uint32_t leaf, int vi, float lo, float sc)
 {
@@ -277,52 +283,41 @@ __device__ __forceinline__ float trilerp(const double v[8], double wx, double wy
     return float(v0 * (1.0 - wz) + v1 * wz);
 }
 
-// One tap of the 9^3 stencil brick of the cached leaf: own block or apron, decoded with the
-// owning block's parameters. All eight taps of a sample are independent loads.
+// The eight taps of a trilinear stencil based at own voxel (x, y, z) in [0, 7]^3 of the cached
+// leaf, in the reference's tap order (sample.hpp:56-63): brick elements e0 + {0, 1, 9, 10, 81, 82,
+// 90, 91} (fixed load offsets). A tap in the apron (its +1 coordinate reaches 8 on the axes in r)
+// decodes with that neighbour block's parameters (lparams[leaf][r]); the taps are independent
+// loads and lanes whose stencils cross a leaf face do not diverge.
 template <int CODEC>
-__device__ __forceinline__ float brick_tap_f(const Accessor<CODEC>& a, int x, int y, int z)
+__device__ __forceinline__ void brick_gather(const Accessor<CODEC>& a, int x, int y, int z, float v[8])
 {
-    SVDB_ASSERT(a.leaf < a.g->n_leaf && unsigned(x) <= 8u && unsigned(y) <= 8u && unsigned(z) <= 8u);
+    SVDB_ASSERT(a.leaf < a.g->n_leaf && unsigned(x) < 8u && unsigned(y) < 8u && unsigned(z) < 8u);
     const uint8_t* base = a.g->codes + size_t(a.leaf) * a.g->leaf_stride;
-    const int r = (x >> 3) | ((y >> 3) << 1) | ((z >> 3) << 2);
-    // The element of the own block / apron region, from per-region coefficient tables, so lanes whose
-    // taps fall in different regions do not diverge: own block (r = 0) x + 8y + 64z; apron region
-    // r packs its remaining axes x-fastest with stride 8 after the 512 own elements.
-    const int xr = x & 7, yr = y & 7, zr = z & 7;
-    const int cy = (0x00180018u >> (4 * r)) & 15;
-    const int cz = (0x01080840u >> (8 * r)) & 255;
-    const int ab = int((0xD8D0C880C0400000ull >> (8 * r)) & 255);
-    const int off = ((~r) & 1) * xr + cy * yr + cz * zr; // element within own block / region
-    if constexpr (CODEC == kCodecF32) {
-        const int e = r ? 512 + ab + off : off;
-        return __ldg(reinterpret_cast<const float*>(base) + e);
-    } else {
-        float lo = a.lo, sc = a.sc;
-        if constexpr (CODEC != kCodecUnorm8) {
-            if (r) {
-                const float2 p = __ldg(a.g->lparams + size_t(a.leaf) * 8 + r);
-                lo = p.x;
-                sc = p.y;
+    const int e0 = brick_index(x, y, z);
+    const int ex = x == 7 ? 1 : 0, ey = y == 7 ? 2 : 0, ez = z == 7 ? 4 : 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int K = (k & 1) + 9 * ((k >> 1) & 1) + 81 * (k >> 2);
+        if constexpr (CODEC == kCodecF32) {
+            v[k] = __ldg(reinterpret_cast<const float*>(base) + e0 + K);
+        } else {
+            float lo = a.lo, sc = a.sc;
+            if constexpr (CODEC != kCodecUnorm8) {
+                const int r = ((k & 1) ? ex : 0) | ((k & 2) ? ey : 0) | ((k & 4) ? ez : 0);
+                if (r) {
+                    const float2 p = __ldg(a.g->lparams + size_t(a.leaf) * 8 + r);
+                    lo = p.x;
+                    sc = p.y;
+                }
+            }
+            if constexpr (CODEC == kCodecAffine4) { // nibble e & 1 of byte e >> 1
+                const int e = e0 + K;
+                v[k] = decode_code<CODEC>((uint32_t(__ldg(base + (e >> 1))) >> ((e & 1) * 4)) & 15u, lo, sc);
+            } else {
+                v[k] = decode_code<CODEC>(__ldg(base + e0 + K), lo, sc);
             }
         }
-        if constexpr (CODEC == kCodecAffine4) {
-            // own block: packed nibbles, the tap's nibble is x's parity (off & 1 == x & 1); apron: one
-            // code per byte, stored in both nibbles (k_build_apron), so the same shift reads it and
-            // the eight taps of a sample need two shift values, not eight
-            const int bi = r ? 256 + ab + off : off >> 1;
-            const int sh = (x & 1) * 4;
-            return decode_code<CODEC>((uint32_t(__ldg(base + bi)) >> sh) & 15u, lo, sc);
-        } else {
-            const int e = r ? 512 + ab + off : off;
-            return decode_code<CODEC>(__ldg(base + e), lo, sc);
-        }
     }
-}
-
-template <int CODEC>
-__device__ __forceinline__ double brick_tap(const Accessor<CODEC>& a, int x, int y, int z)
-{
-    return double(brick_tap_f<CODEC>(a, x, y, z));
 }
 
 template <int CODEC>
@@ -334,11 +329,9 @@ __device__ __forceinline__ float sample_trilinear(Accessor<CODEC>& a, double px,
         float c0;
         if (a.locate(x0, y0, z0, c0)) {
             // base voxel in a leaf: all 8 taps come from that leaf's block + apron
-            const int x = x0 & 7, y = y0 & 7, z = z0 & 7;
-            double v[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                v[k] = brick_tap<CODEC>(a, x + (k & 1), y + ((k >> 1) & 1), z + (k >> 2));
+            float t[8];
+            brick_gather<CODEC>(a, x0 & 7, y0 & 7, z0 & 7, t);
+            const double v[8] = {t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]};
             return trilerp(v, wx, wy, wz);
         }
         // base voxel in a tile / background block (or outside the grid): a non-leaf 8^3 block has

@@ -31,6 +31,26 @@ inline float rd_f32(const uint8_t* p) { float v; std::memcpy(&v, p, 4); return v
 inline bool bit(const uint8_t* words, int i) { return (rd_u64(words + 8 * (i >> 6)) >> (i & 63)) & 1u; }
 
 // ---- K0: leaf codec, one warp per leaf, 128-bit coalesced loads of the staged records ----
+// Own voxel vi (reference order x + 8y + 64z) -> its element of the 9^3 brick (device.cuh)
+__device__ __forceinline__ int brick_of_voxel(int vi) { return brick_index(vi & 7, (vi >> 3) & 7, vi >> 6); }
+constexpr int kBrickA4Bytes = (729 + 1) / 2; // 4-bit brick: 729 nibbles
+
+// 4-bit: write the brick bytes of one leaf from its 512 codes (one per byte, reference order, in
+// shared memory): own nibbles from the codes, apron nibbles 0 (k_build_apron ORs them in)
+__device__ __forceinline__ void write_brick_a4(const uint8_t* s_codes, uint8_t* dst, int lane)
+{
+    for (int i = lane; i < kBrickA4Bytes; i += 32) {
+        uint32_t b = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = 2 * i + h, x = e % 9, y = (e / 9) % 9, z = e / 81;
+            if (e < 729 && x < 8 && y < 8 && z < 8)
+                b |= uint32_t(s_codes[x + 8 * (y + 8 * z)]) << (4 * h);
+        }
+        dst[i] = uint8_t(b);
+    }
+}
+
 template <int CODEC>
 __global__ void __launch_bounds__(256) k_leaf_encode(const uint8_t* __restrict__ staging, uint64_t n_leaf,
                                                      uint8_t* __restrict__ codes_base, uint32_t stride,
@@ -40,35 +60,37 @@ __global__ void __launch_bounds__(256) k_leaf_encode(const uint8_t* __restrict__
     const uint64_t leaf = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
     if (leaf >= n_leaf)
         return;
-    uint8_t* codes = codes_base + leaf * stride; // this leaf's 8^3 block (apron follows it)
+    uint8_t* codes = codes_base + leaf * stride; // this leaf's 9^3 brick (own voxels written here)
     const float4* vals = reinterpret_cast<const float4*>(staging + leaf * kLeafRec + 80);
     float4 v[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
         v[j] = __ldg(vals + j * 32 + lane); // floats [4(32j+lane), +4): 512 B per warp step
     if constexpr (CODEC == kCodecF32) {
-        float4* dst = reinterpret_cast<float4*>(codes);
+        float* dst = reinterpret_cast<float*>(codes);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            dst[j * 32 + lane] = v[j];
+        for (int j = 0; j < 4; ++j) {
+            const int vi = 4 * (j * 32 + lane);
+            dst[brick_of_voxel(vi)] = v[j].x;
+            dst[brick_of_voxel(vi + 1)] = v[j].y;
+            dst[brick_of_voxel(vi + 2)] = v[j].z;
+            dst[brick_of_voxel(vi + 3)] = v[j].w;
+        }
         if (lane == 0)
             params[leaf] = make_float2(0.0f, 0.0f);
         return;
     } else if constexpr (CODEC == kCodecUnorm8) {
-        uint32_t* dst = reinterpret_cast<uint32_t*>(codes);
         bool ok = true;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             float f[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-            uint32_t w = 0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 int c = __float2int_rn(__fmul_rn(f[k], 255.0f));
                 ok &= f[k] >= 0.0f && f[k] <= 1.0f && c >= 0 && c <= 255 &&
                       __double2float_rn(double(c) * (1.0 / 255.0)) == f[k];
-                w |= uint32_t(c & 255) << (8 * k);
+                codes[brick_of_voxel(4 * (j * 32 + lane) + k)] = uint8_t(c & 255);
             }
-            dst[j * 32 + lane] = w;
         }
         if (!ok)
             atomicExch(bad, 1);
@@ -99,40 +121,79 @@ __global__ void __launch_bounds__(256) k_leaf_encode(const uint8_t* __restrict__
             float r = floorf(__fadd_rn(__fdiv_rn(__fsub_rn(x, lo), scale), 0.5f));
             return r < 0.0f ? 0u : (r > float(levels) ? uint32_t(levels) : uint32_t(r));
         };
+        __shared__ uint8_t s_codes[CODEC == kCodecAffine4 ? 8 : 1][512]; // 4-bit: staged per leaf
+        const int w = threadIdx.x >> 5;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            uint32_t c0 = q(v[j].x), c1 = q(v[j].y), c2 = q(v[j].z), c3 = q(v[j].w);
-            if constexpr (CODEC == kCodecAffine8) {
-                reinterpret_cast<uint32_t*>(codes)[j * 32 + lane] =
-                    c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
-            } else {
-                reinterpret_cast<uint16_t*>(codes)[j * 32 + lane] =
-                    uint16_t(c0 | (c1 << 4) | (c2 << 8) | (c3 << 12));
+            const uint32_t c[4] = {q(v[j].x), q(v[j].y), q(v[j].z), q(v[j].w)};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int vi = 4 * (j * 32 + lane) + k;
+                if constexpr (CODEC == kCodecAffine8)
+                    codes[brick_of_voxel(vi)] = uint8_t(c[k]);
+                else
+                    s_codes[w][vi] = uint8_t(c[k]);
             }
+        }
+        if constexpr (CODEC == kCodecAffine4) {
+            __syncwarp();
+            write_brick_a4(s_codes[w], codes, lane);
         }
         if (lane == 0)
             params[leaf] = make_float2(lo, scale);
     }
 }
 
-// SVDB v2 (quantised leaves, `svdbgpu_quantise`): the records already hold the codes and the
-// per-leaf (lo, scale); copy them into the strided device layout, 8 B per lane step.
+// SVDB v2 (quantised leaves, `svdbgpu_quantise`): the records already hold the codes (reference
+// voxel order) and the per-leaf (lo, scale); place the codes in the leaf's 9^3 brick.
 // Record: origin/pad 16 B | active mask 64 B | lo, scale 8 B | codes main_bytes.
+template <int CODEC>
 __global__ void __launch_bounds__(256) k_leaf_load(const uint8_t* __restrict__ staging, uint64_t n_leaf,
-                                                   uint32_t rec, uint32_t main_bytes, uint8_t* __restrict__ codes_base,
-                                                   uint32_t stride, float2* __restrict__ params)
+                                                   uint32_t rec, uint8_t* __restrict__ codes_base, uint32_t stride,
+                                                   float2* __restrict__ params)
 {
-    const int lane = threadIdx.x & 31;
-    const uint64_t leaf = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    __shared__ uint8_t s_codes[8][512];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t leaf = uint64_t(blockIdx.x) * 8 + w;
     if (leaf >= n_leaf)
         return;
-    const uint8_t* r = staging + leaf * rec;
-    const uint2* s2 = reinterpret_cast<const uint2*>(r + 88);
-    uint2* d2 = reinterpret_cast<uint2*>(codes_base + leaf * stride);
-    for (uint32_t i = lane; i < main_bytes / 8; i += 32)
-        d2[i] = __ldg(s2 + i);
+    const uint8_t* r = staging + leaf * rec + 88;
+    uint8_t* dst = codes_base + leaf * stride;
+    if constexpr (CODEC == kCodecAffine4) {
+        for (int vi = lane; vi < 512; vi += 32)
+            s_codes[w][vi] = uint8_t((__ldg(r + (vi >> 1)) >> ((vi & 1) * 4)) & 15u);
+        __syncwarp();
+        write_brick_a4(s_codes[w], dst, lane);
+    } else {
+        for (int vi = lane; vi < 512; vi += 32)
+            dst[brick_of_voxel(vi)] = __ldg(r + vi);
+    }
     if (lane == 0)
-        params[leaf] = *reinterpret_cast<const float2*>(r + 80);
+        params[leaf] = *reinterpret_cast<const float2*>(staging + leaf * rec + 80);
+}
+
+// The own codes of leaves [first, first + count) in the reference voxel order (main_bytes per
+// leaf; the inverse of the brick placement), for the v2 container
+template <int CODEC>
+__global__ void k_leaf_unbrick(DevGrid g, uint64_t first, uint64_t count, uint8_t* __restrict__ out)
+{
+    const uint64_t n = count * 512;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t l = i >> 9;
+        const int vi = int(i & 511), e = brick_of_voxel(vi);
+        const uint8_t* src = g.codes + (first + l) * g.leaf_stride;
+        if constexpr (CODEC == kCodecF32) {
+            reinterpret_cast<float*>(out)[i] = reinterpret_cast<const float*>(src)[e];
+        } else if constexpr (CODEC == kCodecAffine4) {
+            if (vi & 1)
+                continue;
+            const uint32_t c0 = (src[e >> 1] >> ((e & 1) * 4)) & 15u, e1 = brick_of_voxel(vi + 1);
+            const uint32_t c1 = (src[e1 >> 1] >> ((e1 & 1) * 4)) & 15u;
+            out[l * 256 + (vi >> 1)] = uint8_t(c0 | (c1 << 4));
+        } else {
+            out[i] = src[e];
+        }
+    }
 }
 
 // Lower slot table with the child leaf's decode parameters folded in (one 16-B load per miss).
@@ -221,13 +282,14 @@ __global__ void __launch_bounds__(256) k_build_apron(DevGrid g, const int4* __re
     __syncwarp();
     if (!live)
         return;
-    uint8_t* dst = const_cast<uint8_t*>(g.codes) + leaf * g.leaf_stride + g.main_bytes;
+    uint8_t* dst = const_cast<uint8_t*>(g.codes) + leaf * g.leaf_stride;
     bool ok = true;
-    for (int e = lane; e < 217; e += 32) {
+    for (int a = lane; a < 217; a += 32) {
         int r, x, y, z;
-        apron_entry(e, r, x, y, z);
+        apron_entry(a, r, x, y, z); // (x, y, z): the voxel in the neighbour block r
         const uint4 info = s_info[w][r];
-        const int vi = x + 8 * (y + 8 * z);
+        const int vi = brick_index(x, y, z); // its element in the neighbour's brick
+        const int e = brick_index(r & 1 ? 8 : x, r & 2 ? 8 : y, r & 4 ? 8 : z); // and in this one
         const uint8_t* nb = g.codes + size_t(info.y) * g.leaf_stride;
         const float cval = __uint_as_float(info.y);
         if constexpr (CODEC == kCodecF32) {
@@ -241,8 +303,10 @@ __global__ void __launch_bounds__(256) k_build_apron(DevGrid g, const int4* __re
                 ok &= q >= 0 && q <= 255 && __double2float_rn(double(q) * (1.0 / 255.0)) == cval;
                 c = uint32_t(q & 255);
             }
-            // 4-bit: the code in both nibbles, so a tap's nibble shift depends on its x parity only
-            dst[e] = uint8_t(CODEC == kCodecAffine4 ? c * 17u : c);
+            if constexpr (CODEC == kCodecAffine4) // nibble e & 1 of byte e >> 1: OR into its word
+                atomicOr(reinterpret_cast<unsigned*>(dst) + (e >> 3), c << (((e >> 1) & 3) * 8 + (e & 1) * 4));
+            else
+                dst[e] = uint8_t(c);
         }
     }
     if (!ok)
@@ -671,7 +735,8 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
     if (resolved == SVDBGPU_CODEC_AUTO8)
         resolved = vt == 0 ? kCodecUnorm8 : kCodecAffine8;
     const uint32_t main_bytes = resolved == kCodecF32 ? 2048u : (resolved == kCodecAffine4 ? 256u : 512u);
-    const uint32_t stride = main_bytes + (resolved == kCodecF32 ? 880u : 256u); // + 217-entry apron
+    // the 9^3 brick (729 elements) per leaf, padded to a multiple of 128 B
+    const uint32_t stride = resolved == kCodecF32 ? 2944u : (resolved == kCodecAffine4 ? 384u : 768u);
     float2* d_params = nullptr;
     uint2* d_lstage = nullptr;
     uint8_t* d_stage = nullptr;
@@ -713,7 +778,10 @@ int grid_create(const uint8_t* b, size_t n, int codec, int device, GridImpl** ou
             uint8_t* dst = g->d_codes + size_t(stride) * first;
             float2* par = d_params + first;
             if (stored >= 0) {
-                k_leaf_load<<<blocks, 256, 0, s>>>(d_stage, cnt, uint32_t(leaf_rec), main_bytes, dst, stride, par);
+                if (stored == kCodecAffine4)
+                    k_leaf_load<kCodecAffine4><<<blocks, 256, 0, s>>>(d_stage, cnt, uint32_t(leaf_rec), dst, stride, par);
+                else
+                    k_leaf_load<kCodecAffine8><<<blocks, 256, 0, s>>>(d_stage, cnt, uint32_t(leaf_rec), dst, stride, par);
             } else {
 #define LAUNCH_ENCODE(C) k_leaf_encode<C><<<blocks, 256, 0, s>>>(d_stage, cnt, dst, stride, par, d_bad)
                 SVDB_CODEC_DISPATCH(resolved, LAUNCH_ENCODE)
@@ -789,9 +857,24 @@ int grid_leaf_codes(const GridImpl* g, uint64_t first, uint64_t count, uint8_t* 
     if (first + count > g->n_leaf)
         return fail_code(SVDBGPU_E_INVALID_ARG, "leaf range out of bounds");
     SVDB_CUDA(cudaSetDevice(g->device));
-    if (codes && count) // the leaf's own 8^3 block (the apron behind it is derived data)
-        SVDB_CUDA(cudaMemcpy2D(codes, g->dg.main_bytes, g->d_codes + size_t(g->dg.leaf_stride) * first,
-                               g->dg.leaf_stride, g->dg.main_bytes, count, cudaMemcpyDeviceToHost));
+    if (codes && count) { // the leaves' own 8^3 blocks out of their bricks (the apron is derived data)
+        const uint64_t step = std::min<uint64_t>(count, 1ull << 18);
+        uint8_t* d_out = nullptr;
+        SVDB_CUDA(cudaMalloc(&d_out, size_t(step) * g->dg.main_bytes));
+        for (uint64_t f = 0; f < count; f += step) {
+            const uint64_t c = std::min(step, count - f);
+#define LAUNCH_UNBRICK(C) k_leaf_unbrick<C><<<grid_blocks(c * 512), 256>>>(g->dg, first + f, c, d_out)
+            SVDB_CODEC_DISPATCH(g->codec, LAUNCH_UNBRICK)
+#undef LAUNCH_UNBRICK
+            const cudaError_t e = cudaMemcpy(codes + size_t(f) * g->dg.main_bytes, d_out, size_t(c) * g->dg.main_bytes,
+                                             cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) {
+                cudaFree(d_out);
+                SVDB_CUDA(e);
+            }
+        }
+        cudaFree(d_out);
+    }
     if (params && count) {
         // params live folded in the lower table; recover them by scanning it on the host
         std::vector<uint4> low(size_t(g->n_lower) * 4096);

@@ -41,8 +41,8 @@ struct DevGrid {
     const uint4* lower;
     const uint8_t* codes;
     float2* lparams;      // 8 x (lo, scale) per leaf: [0] own, [1..7] apron regions
-    uint32_t leaf_stride; // bytes per leaf: own block (main_bytes) + 217-entry apron
-    uint32_t main_bytes;  // 2048 f32, 512 u8, 256 u4
+    uint32_t leaf_stride; // bytes per leaf: the 9^3 stencil brick (own 8^3 block + 217-voxel apron)
+    uint32_t main_bytes;  // the own block in the reference's voxel order (v2 container): 2048 f32, 512 u8, 256 u4
     uint32_t n_leaf, n_lower;
     // leaf directory: for every 8^3 block of [0, 8*dir_dims) the root->upper->lower walk resolved
     // at build time ({kind, payload, lo, scale} as in `lower`; tile / background as kind tile with

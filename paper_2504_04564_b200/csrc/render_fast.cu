@@ -124,10 +124,7 @@ __device__ __forceinline__ float sample_f(Accessor<CODEC>& a, G px, G py, G pz)
     float v[8];
     float c0;
     if (a.locate(x0, y0, z0, c0)) {
-        const int x = x0 & 7, y = y0 & 7, z = z0 & 7;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            v[k] = brick_tap_f<CODEC>(a, x + (k & 1), y + ((k >> 1) & 1), z + (k >> 2));
+        brick_gather<CODEC>(a, x0 & 7, y0 & 7, z0 & 7, v);
     } else {
         v[0] = c0;
 #pragma unroll 1
