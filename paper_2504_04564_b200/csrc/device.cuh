@@ -341,11 +341,13 @@ __device__ __forceinline__ float sample_trilinear(Accessor<CODEC>& a, double px,
         const int cross = ((x0 & 7) == 7 ? 1 : 0) | ((y0 & 7) == 7 ? 2 : 0) | ((z0 & 7) == 7 ? 4 : 0);
         float t[8] = {c0, c0, c0, c0, c0, c0, c0, c0}; // taps are floats (sample.hpp:56-63)
         if (cross) {
-            // one copy of the lookup in the instruction stream (rolled), results into registers
+            // one copy of the lookup in the instruction stream (rolled) over the taps across the
+            // faces only (mask of i with i & cross != 0, from a table), results into registers
+            unsigned m = unsigned(0xFEFCFAF0EECCAA00ull >> (8 * cross)) & 0xFEu;
 #pragma unroll 1
-            for (int i = 1; i < 8; ++i) {
-                if (!(i & cross))
-                    continue;
+            while (m) {
+                const int i = __ffs(m) - 1;
+                m &= m - 1u;
                 const float r = a.read_located(x0 + (i & 1), y0 + ((i >> 1) & 1), z0 + (i >> 2));
                 switch (i) {
                 case 1: t[1] = r; break;
