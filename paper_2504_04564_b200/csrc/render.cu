@@ -476,10 +476,14 @@ __global__ void __launch_bounds__(256) k_render(const __grid_constant__ RenderAr
 // the image is bit-identical to k_render and to the CPU oracles. Pixels are handed out in 8x4
 // blocks per warp from a global counter (lanes refill individually, so no lane idles at a pixel
 // boundary); the grid is sized to the resident CTA count.
-enum : int { kNeedPixel = 0, kNeedPath = 1, kNeedSegment = 2, kNeedCell = 3, kInCell = 4, kPoint = 5, kScatter = 6,
-             kNeedRegion = 7, // hierarchical DDA: next 128^3 lower-node region
-             kNeedLog = 8,    // tentative step whose cell-exit decision needs the exact FP64 log
-             kEscape = 9 };   // flight over (left the grid / Tr = 0): result written in the start phase
+// state >> 2 is the lane's phase group: 0 idle (needs a work item), 1 start, 2 advance, 3 gather
+enum : int { kNeedPixel = 0,
+             kNeedPath = 4, kNeedSegment = 5, kScatter = 6,
+             kEscape = 7, // flight over (left the grid / Tr = 0): result written in the start phase
+             kNeedCell = 8, kInCell = 9,
+             kNeedRegion = 10, // hierarchical DDA: next 128^3 lower-node region
+             kPoint = 12,
+             kNeedLog = 13 }; // tentative step whose cell-exit decision needs the exact FP64 log   // flight over (left the grid / Tr = 0): result written in the start phase
 
 // The macrocell DDA of device.cuh (dda.hpp:52-109), same arithmetic, with its 23 words of
 // per-lane state in shared memory (SoA, conflict-free) instead of registers: it is touched once
@@ -1127,10 +1131,10 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         // ---- phase selection: run the one phase most lanes are waiting in; ties go to the
         // gather so its memory latency is paid by as many lanes as possible at once. Finished
         // lanes stay in kNeedPixel, which is in no phase ----
-        const int nS = __popc(__ballot_sync(FULL, state == kPoint || state == kNeedLog));
-        const int nA = __popc(__ballot_sync(FULL, state == kNeedCell || state == kInCell || state == kNeedRegion));
-        const int nT = __popc(__ballot_sync(FULL, state == kNeedPath || state == kNeedSegment || state == kScatter ||
-                                                      state == kEscape));
+        const int group = state >> 2;
+        const int nS = __popc(__ballot_sync(FULL, group == 3));
+        const int nA = __popc(__ballot_sync(FULL, group == 2));
+        const int nT = __popc(__ballot_sync(FULL, group == 1));
         if (nS + nA + nT == 0) { // every lane waits for a work item (none left: the warp is done)
             if (__all_sync(FULL, done))
                 break;
@@ -1153,11 +1157,11 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         }
 #endif
         if (phase == 0) {
-            if (state == kNeedPath || state == kNeedSegment || state == kScatter || state == kEscape)
+            if (group == 1)
                 do_start();
         } else if (phase == 1) {
 #pragma unroll 1
-            for (int k = 0; k < kAdvIters && (state == kNeedCell || state == kInCell || state == kNeedRegion); ++k)
+            for (int k = 0; k < kAdvIters && (state >> 2) == 2; ++k)
                 do_advance();
         } else {
             if (state == kNeedLog)
