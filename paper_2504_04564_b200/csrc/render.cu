@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     volatile int& have_d = s_cold_i[RATIO ? 6 : 0][tid];              // ratio: event pending (0/1)
     volatile int& s_end = s_cold_i[CHUNK ? (RATIO ? 7 : 6) : 0][tid]; // chunked: end of the lane's samples
     volatile int &px = s_cold_i[0][tid], &py = s_cold_i[1][tid], &s = s_cold_i[2][tid];
-    volatile int &bounces = s_cold_i[3][tid], &out_off = s_cold_i[4][tid];
+    volatile int &bounces = s_cold_i[3][tid], &out_off = s_cold_i[4][tid]; // see the work hand-out
     volatile float& v_ev = reinterpret_cast<volatile float&>(s_cold_i[5][tid]);
     struct HaveRef {
         volatile int& d;
@@ -775,8 +775,8 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     // path finished with float result r (render.hpp:306: accum += Vec3d(c))
     auto finish_path = [&](float r0, float r1, float r2) {
         if constexpr (CHUNK) { // the sample's result, summed in order by k_reduce
-            SVDB_ASSERT(out_off / 3 < A.npix && s < A.spp);
-            float* o = A.sbuf + (size_t(out_off / 3) * size_t(A.spp) + size_t(s)) * 3;
+            SVDB_ASSERT(out_off / A.spp < A.npix && s < A.spp);
+            float* o = A.sbuf + (size_t(out_off) + size_t(s)) * 3; // out_off = pixel * spp (chunked)
             o[0] = r0;
             o[1] = r1;
             o[2] = r2;
@@ -874,8 +874,8 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             bool from_table = false;
             if constexpr (CHUNK) {
                 if (A.camtab) { // ray and post-jitter stream from k_camera_rays (same arithmetic)
-                    SVDB_ASSERT(out_off / 3 < A.npix && s < A.spp);
-                    const double2* rec = A.camtab + 2 * (size_t(out_off / 3) * size_t(A.spp) + size_t(s));
+                    SVDB_ASSERT(out_off / A.spp < A.npix && s < A.spp);
+                    const double2* rec = A.camtab + 2 * (size_t(out_off) + size_t(s));
                     const double2 a = __ldg(rec), b = __ldg(rec + 1);
                     rng.state = uint64_t(__double_as_longlong(b.y));
                     Ray r;
@@ -1113,7 +1113,10 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
                 px = int(tt % A.tiles_x) * 16 + lx;
                 py = int(tt / A.tiles_x) * 16 + ly;
                 if (px < A.cam.w && py < A.cam.h) {
-                    out_off = A.packed ? (k * 256 + ly * 16 + lx) * 3 : ((long long)py * A.cam.w + px) * 3;
+                    const long long pix = A.packed ? k * 256 + ly * 16 + lx : (long long)py * A.cam.w + px;
+                    // whole-pixel items: the pixel's first float in the image; chunked items: the
+                    // pixel's first per-sample slot (pixel * spp < 2^31: the per-sample buffer is capped)
+                    out_off = int(CHUNK ? pix * A.spp : pix * 3);
                     if constexpr (CHUNK) {
                         s = j * A.chunk;
                         s_end = min(A.spp, (j + 1) * A.chunk);
