@@ -461,15 +461,6 @@ struct Rng {
         h = mix64(h ^ uint64_t(uint32_t(s)));
         return Rng{mix64(h)};
     }
-    // the next uniform() value without consuming it (pure function of the state)
-    __device__ __forceinline__ double peek() const
-    {
-        uint64_t x = state + 0x9E3779B97F4A7C15ull;
-        x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-        x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-        x ^= x >> 31;
-        return double(x >> 11) * 0x1.0p-53;
-    }
     // the 53 random bits of the next uniform() (u = bits * 2^-53), not consumed
     __device__ __forceinline__ uint64_t peek_bits() const
     {
