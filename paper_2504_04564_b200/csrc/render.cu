@@ -662,10 +662,13 @@ struct SharedDda {
         // the stepped axis' values by selects on the two comparisons (tn is already t_next[axis])
         const int c = (ax2 ? c2 : (ax1 ? c1 : c0)) + stepv(axis);
         ci(axis) = c;
-        const int lo_a = RANGED ? (ax2 ? lo[2] : (ax1 ? lo[1] : lo[0])) : 0;
-        const int hi_a = RANGED ? (ax2 ? hi[2] : (ax1 ? hi[1] : hi[0])) : cells[axis] - 1;
-        if (c < lo_a || c > hi_a)
+        if constexpr (RANGED) {
+            const int lo_a = ax2 ? lo[2] : (ax1 ? lo[1] : lo[0]), hi_a = ax2 ? hi[2] : (ax1 ? hi[1] : hi[0]);
+            if (c < lo_a || c > hi_a)
+                return;
+        } else if (unsigned(c) >= unsigned(ax2 ? cells[2] : (ax1 ? cells[1] : cells[0]))) { // selects, not an indexed constant load
             return;
+        }
         cd(axis) = tn + cd(3 + axis);
         c0 = axis == 0 ? c : c0;
         c1 = axis == 1 ? c : c1;
