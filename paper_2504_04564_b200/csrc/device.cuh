@@ -325,44 +325,42 @@ __device__ __forceinline__ float sample_trilinear(Accessor<CODEC>& a, double px,
 {
     const int x0 = lattice_coord(px), y0 = lattice_coord(py), z0 = lattice_coord(pz);
     const double wx = px - floor(px), wy = py - floor(py), wz = pz - floor(pz);
-    {
-        float c0;
-        if (a.locate(x0, y0, z0, c0)) {
-            // base voxel in a leaf: all 8 taps come from that leaf's block + apron
-            float t[8];
-            brick_gather<CODEC>(a, x0 & 7, y0 & 7, z0 & 7, t);
-            const double v[8] = {t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]};
-            return trilerp(v, wx, wy, wz);
-        }
+    float t[8]; // the taps are floats (sample.hpp:56-63); both branches fill them and the lanes
+                // reconverge for one copy of the FP64 interpolation
+    float c0;
+    if (a.locate(x0, y0, z0, c0)) {
+        // base voxel in a leaf: all 8 taps come from that leaf's brick
+        brick_gather<CODEC>(a, x0 & 7, y0 & 7, z0 & 7, t);
+    } else {
         // base voxel in a tile / background block (or outside the grid): a non-leaf 8^3 block has
         // one value, so every tap inside the base block is c0 with no load; only taps across the
         // block's far faces are looked up (through the leaf directory, independent loads). Tap
         // order as sample.hpp:56-63.
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            t[k] = c0;
         const int cross = ((x0 & 7) == 7 ? 1 : 0) | ((y0 & 7) == 7 ? 2 : 0) | ((z0 & 7) == 7 ? 4 : 0);
-        float t[8] = {c0, c0, c0, c0, c0, c0, c0, c0}; // taps are floats (sample.hpp:56-63)
-        if (cross) {
-            // one copy of the lookup in the instruction stream (rolled) over the taps across the
-            // faces only (mask of i with i & cross != 0, from a table), results into registers
-            unsigned m = unsigned(0xFEFCFAF0EECCAA00ull >> (8 * cross)) & 0xFEu;
+        // one copy of the lookup in the instruction stream (rolled) over the taps across the faces
+        // only (mask of i with i & cross != 0, from a table), results into registers
+        unsigned m = unsigned(0xFEFCFAF0EECCAA00ull >> (8 * cross)) & 0xFEu;
 #pragma unroll 1
-            while (m) {
-                const int i = __ffs(m) - 1;
-                m &= m - 1u;
-                const float r = a.read_located(x0 + (i & 1), y0 + ((i >> 1) & 1), z0 + (i >> 2));
-                switch (i) {
-                case 1: t[1] = r; break;
-                case 2: t[2] = r; break;
-                case 3: t[3] = r; break;
-                case 4: t[4] = r; break;
-                case 5: t[5] = r; break;
-                case 6: t[6] = r; break;
-                default: t[7] = r; break;
-                }
+        while (m) {
+            const int i = __ffs(m) - 1;
+            m &= m - 1u;
+            const float r = a.read_located(x0 + (i & 1), y0 + ((i >> 1) & 1), z0 + (i >> 2));
+            switch (i) {
+            case 1: t[1] = r; break;
+            case 2: t[2] = r; break;
+            case 3: t[3] = r; break;
+            case 4: t[4] = r; break;
+            case 5: t[5] = r; break;
+            case 6: t[6] = r; break;
+            default: t[7] = r; break;
             }
         }
-        const double v[8] = {t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]};
-        return trilerp(v, wx, wy, wz);
     }
+    const double v[8] = {t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]};
+    return trilerp(v, wx, wy, wz);
 }
 
 template <int CODEC>
