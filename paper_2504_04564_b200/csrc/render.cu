@@ -791,16 +791,11 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         ++s;
         state = kNeedPath;
     };
-    auto finish_ratio = [&]() { finish_path(float(L0), float(L1), float(L2)); };
-    // scattering vertex (render.hpp:173-185)
-    auto bounce = [&](double te, float ve) {
-        if (++bounces > A.max_bounces) {
-            if constexpr (RATIO)
-                finish_ratio();
-            else
-                finish_path(0.0f, 0.0f, 0.0f);
-            return;
-        }
+    // scattering vertex (render.hpp:173-185); returns 0 when the path continues (state
+    // kNeedSegment), else how it ended: 2 absorbed (max bounces / Russian roulette), ratio 3
+    auto bounce = [&](double te, float ve) -> int {
+        if (++bounces > A.max_bounces)
+            return RATIO ? 3 : 2;
         double tpv[3] = {tp0, tp1, tp2};
         tr.scatter_albedo(ve, tpv);
         tp0 = tpv[0];
@@ -816,34 +811,15 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         }
         if (bounces >= A.rr_start) {
             double survive = dclamp(dmax(tp0, dmax(tp1, tp2)), 0.05, 0.95);
-            if (rng.uniform() >= survive) {
-                if constexpr (RATIO)
-                    finish_ratio();
-                else
-                    finish_path(0.0f, 0.0f, 0.0f);
-                return;
-            }
+            if (rng.uniform() >= survive)
+                return RATIO ? 3 : 2;
             const double ys = 1.0 / survive; // render.hpp:184, tp /= survive per channel, exactly
 #pragma unroll
             for (int k = 0; k < 3; ++k)
                 s_cold_d[kA + k][tid] = div_by_rcp(s_cold_d[kA + k][tid], survive, ys);
         }
         state = kNeedSegment;
-    };
-    // the flight left the grid (or Tr hit 0): escape / ratio segment end
-    auto end_segment = [&]() {
-        if constexpr (RATIO) {
-            L0 += tp0 * Tr * double(A.ambient[0]);
-            L1 += tp1 * Tr * double(A.ambient[1]);
-            L2 += tp2 * Tr * double(A.ambient[2]);
-            if (!have)
-                finish_ratio();
-            else
-                state = kScatter;
-        } else {
-            finish_path(float(tp0 * double(A.ambient[0])), float(tp1 * double(A.ambient[1])),
-                        float(tp2 * double(A.ambient[2])));
-        }
+        return 0;
     };
     // a flight that ran out of cells (or of transmittance) ends in the start phase, batched with
     // the other lanes writing results and starting paths, instead of inside the advance / gather
@@ -853,13 +829,38 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
     // start the next sample (render.hpp:298-302), or enter the macrocell DDA with a new flight
     // (render.hpp:142)
     auto do_start = [&]() {
-        if (state == kEscape)
-            end_segment();
-        if (state == kScatter) { // the only copy of the scattering code in the loop
-            bounce(t_ev, v_ev);
-            if (state == kNeedSegment)
-                goto segment;
+        // how the flight / path ended: 1 escaped (result tp * ambient), 2 absorbed (0), 3 ratio (L)
+        int fin = 0;
+        if (state == kEscape) { // the flight left the grid (or Tr hit 0): escape / ratio segment end
+            if constexpr (RATIO) {
+                L0 += tp0 * Tr * double(A.ambient[0]);
+                L1 += tp1 * Tr * double(A.ambient[1]);
+                L2 += tp2 * Tr * double(A.ambient[2]);
+                if (have)
+                    state = kScatter;
+                else
+                    fin = 3;
+            } else {
+                fin = 1;
+            }
         }
+        if (state == kScatter) // the only copy of the scattering code in the loop
+            fin = bounce(t_ev, v_ev);
+        if (fin) { // the one result write (render.hpp:306)
+            float r0 = 0.0f, r1 = 0.0f, r2 = 0.0f;
+            if constexpr (RATIO) {
+                r0 = float(L0);
+                r1 = float(L1);
+                r2 = float(L2);
+            } else if (fin == 1) {
+                r0 = float(tp0 * double(A.ambient[0]));
+                r1 = float(tp1 * double(A.ambient[1]));
+                r2 = float(tp2 * double(A.ambient[2]));
+            }
+            finish_path(r0, r1, r2);
+        }
+        if (state == kNeedSegment)
+            goto segment;
         if (state == kNeedPath) {
             if constexpr (CHUNK) {
                 if (s == s_end) { // sample range done; k_reduce writes the pixel
@@ -924,7 +925,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
 #endif
         if constexpr (HDDA) {
             if (!rdda.init(A.ccells, A.hi, ray_load(), 0.0, kInf(), 128.0, 1.0 / 128.0)) {
-                end_segment();
+                flight_over(); // missed the grid: the segment ends (next start phase)
                 return;
             }
             r_entry = -1;
@@ -932,7 +933,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
             return;
         }
         if (!dda.init(A.cells, A.hi, ray_load(), 0.0, kInf(), A.cell, A.icell)) {
-            end_segment();
+            flight_over(); // missed the grid: the segment ends (next start phase)
             return;
         }
         tb = dda.cd(6); // the walk position (next_ahead)
