@@ -2,6 +2,8 @@
 background), random transfer functions, cameras (outside, inside, grazing) and settings, rendered
 on the B200 and by the unmodified reference (pathtrace / iso) or the C restatement (ea / ratio),
 plus random sample positions through the sampler. Seeds are fixed, so failures reproduce."""
+import os
+
 import numpy as np
 import pytest
 
@@ -47,7 +49,7 @@ def _random_case(ref, seed):
     return svdb, tf, cam, st
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SVDB_RANDOM_SEEDS", "24"))))  # wider sweeps: env
 def test_random_scene_parity(gpu, ref, orc, seed):
     svdb, tf, cam, st = _random_case(ref, 1000 + seed)
     g = P.DeviceGrid(svdb, P.Codec.f32)
@@ -73,7 +75,7 @@ def test_random_samples_bit_exact(gpu, ref, seed):
     assert np.array_equal(bits(got), bits(want))
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SVDB_RANDOM_QSEEDS", "8"))))
 def test_random_quantised_scene_parity(gpu, ref, orc, seed):
     # N-bit leaves: the oracle image is the reference on the dequantised SVDB
     svdb, tf, cam, st = _random_case(ref, 3000 + seed)
