@@ -952,8 +952,10 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         // the integer to float then scaling by a power of two is the same RN(1 - u) (no FP64 ops)
         float one_minus_u = __ull2float_rn((1ull << 53) - rng.peek_bits()) * 0x1p-53f, lg;
         asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(one_minus_u)); // normal argument (>= 2^-53)
-        const float y = -lg * 0.693147182f;
-        const float y_lb = y - (4e-6f + 4e-6f * y);
+        // lower bound of y = -ln(1 - u), margins 4e-6 absolute and 4e-6 relative, pre-scaled by
+        // 0.999998 (the decision's 1e-6 relative margins on each side) so the test below is one
+        // product: y_lb = lg * (-ln 2 (1 - 4e-6) 0.999998, rounded towards 0) - 4e-6, in one FMA
+        const float y_lb = __fmaf_rn(lg, -0x1.62e3a4p-1f, -4e-6f);
         if constexpr (HDDA) {
             if (state == kNeedRegion) { // next lower-node region; one without draws is skipped whole
                 int rc[3];
@@ -1041,7 +1043,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks) k_trace(const 
         // When the float bound already clears the gap with margin (>= 1e-6 relative, far above every
         // rounding error) the decision is certain: no FP64 log. Otherwise the exact step is taken in
         // the gather phase (kNeedLog), batched with the collisions it mostly leads to.
-        if (y_lb * float(inv) * 0.999999f > float(tb - t) * 1.000001f) {
+        if (y_lb * float(inv) > float(tb - t)) {
             state = kNeedCell;
             return;
         }
